@@ -1,0 +1,827 @@
+// libvtensor.so — the vTensor device shim (C ABI in include/vtensor.h).
+//
+// Two layers in one object:
+//   1. A bookkeeping state machine that is bit-exact with the reference's
+//      simulated device (kvsim/device.py:118-295): monotone never-reused
+//      ordinals for range bases (device.py:199-201) and handle ids
+//      (device.py:212-213), byte accounting (device.py:141-182), the
+//      instrumented call log (device.py:184-187) and the nine error classes.
+//      Ordering decisions never depend on real CUdeviceptr or CUDA handle
+//      values, so manager state stays identical to the oracle.
+//   2. On a GPU, a CUDA-driver VMM backend. reserve runs inline (the VA must
+//      be known immediately); create/map/unmap/destroy/release are queued in
+//      issue order to a per-device worker thread so chunk mapping overlaps the
+//      decode kernels (north_star item 1). OOM is decided by the configured
+//      byte budget (device.py:153-160, 208-211), never by the driver.
+//
+// The driver is loaded with dlopen at first use: the CPU CI container has no
+// libcuda.so.1, and the simulated backend must work there.
+
+#include "../../include/vtensor.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// ---------------------------------------------------------------------------
+// Driver entry points (resolved once with dlopen/dlsym).
+// ---------------------------------------------------------------------------
+struct Driver {
+  bool loaded = false;
+  std::string error;
+  CUresult (*Init)(unsigned int);
+  CUresult (*DeviceGet)(CUdevice*, int);
+  CUresult (*PrimaryCtxRetain)(CUcontext*, CUdevice);
+  CUresult (*CtxSetCurrent)(CUcontext);
+  CUresult (*CtxGetCurrent)(CUcontext*);
+  CUresult (*AddrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*AddrFree)(CUdeviceptr, size_t);
+  CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                        unsigned long long);
+  CUresult (*MemRelease)(CUmemGenericAllocationHandle);
+  CUresult (*MemMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle,
+                     unsigned long long);
+  CUresult (*MemUnmap)(CUdeviceptr, size_t);
+  CUresult (*MemSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*Granularity)(size_t*, const CUmemAllocationProp*,
+                          CUmemAllocationGranularity_flags);
+  CUresult (*EventCreate)(CUevent*, unsigned int);
+  CUresult (*EventRecord)(CUevent, CUstream);
+  CUresult (*EventSynchronize)(CUevent);
+  CUresult (*EventDestroy)(CUevent);
+  CUresult (*GetErrorString)(CUresult, const char**);
+  CUresult (*TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+};
+
+Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcuda.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      d.error = std::string("cannot dlopen libcuda.so.1: ") + dlerror();
+      return;
+    }
+    bool ok = true;
+    auto sym = [&](const char* name) -> void* {
+      void* p = dlsym(h, name);
+      if (!p) {
+        ok = false;
+        d.error += std::string("missing driver symbol ") + name + "; ";
+      }
+      return p;
+    };
+#define VT_SYM(field, name) d.field = reinterpret_cast<decltype(d.field)>(sym(name))
+    VT_SYM(Init, "cuInit");
+    VT_SYM(DeviceGet, "cuDeviceGet");
+    VT_SYM(PrimaryCtxRetain, "cuDevicePrimaryCtxRetain");
+    VT_SYM(CtxSetCurrent, "cuCtxSetCurrent");
+    VT_SYM(CtxGetCurrent, "cuCtxGetCurrent");
+    VT_SYM(AddrReserve, "cuMemAddressReserve");
+    VT_SYM(AddrFree, "cuMemAddressFree");
+    VT_SYM(MemCreate, "cuMemCreate");
+    VT_SYM(MemRelease, "cuMemRelease");
+    VT_SYM(MemMap, "cuMemMap");
+    VT_SYM(MemUnmap, "cuMemUnmap");
+    VT_SYM(MemSetAccess, "cuMemSetAccess");
+    VT_SYM(Granularity, "cuMemGetAllocationGranularity");
+    VT_SYM(EventCreate, "cuEventCreate");
+    VT_SYM(EventRecord, "cuEventRecord");
+    VT_SYM(EventSynchronize, "cuEventSynchronize");
+    VT_SYM(EventDestroy, "cuEventDestroy_v2");
+    VT_SYM(GetErrorString, "cuGetErrorString");
+    VT_SYM(TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
+#undef VT_SYM
+    if (ok && d.Init(0) != CUDA_SUCCESS) {
+      ok = false;
+      d.error += "cuInit failed; ";
+    }
+    d.loaded = ok;
+  });
+  return d;
+}
+
+std::string cu_err(CUresult r) {
+  const char* s = nullptr;
+  if (driver().GetErrorString) driver().GetErrorString(r, &s);
+  return s ? std::string(s) : ("CUresult " + std::to_string(static_cast<int>(r)));
+}
+
+// ---------------------------------------------------------------------------
+// Worker-side driver ops.
+// ---------------------------------------------------------------------------
+enum class DrvKind : uint8_t { kCreate, kMap, kUnmap, kDestroy, kRelease };
+
+struct DrvOp {
+  DrvKind kind;
+  int64_t handle_id;     // create / map / destroy
+  CUdeviceptr addr;      // map / unmap / release
+  size_t size;           // release
+  uint64_t fence_epoch;  // teardown ops wait for this stream event
+  uint64_t ticket;
+  int64_t submit_ns;
+};
+
+constexpr int kFenceRing = 64;
+
+}  // namespace
+
+// One reserved range: its page -> handle-id table (-1 = unmapped).
+struct RangeState {
+  int64_t pages = 0;
+  int64_t mapped = 0;
+  std::vector<int64_t> slot;
+  CUdeviceptr va = 0;
+};
+
+struct vt_device {
+  vt_config cfg{};
+  int ordinal = -1;  // <0: simulated
+  std::string last_error;
+
+  // --- bookkeeping state machine (device.py:127-137) ---
+  std::map<int64_t, RangeState> ranges;               // ordered: live_ranges() sorted
+  std::map<int64_t, int64_t> handles;                 // id -> map_count, ordered
+  int64_t next_base = 0;
+  int64_t next_handle = 0;
+  int64_t mapped_pages = 0;
+  int64_t active_requests = 0;
+  int64_t reserved_bytes = 0;
+  std::vector<vt_call> log;
+
+  // --- CUDA backend ---
+  CUcontext ctx = nullptr;
+  CUmemAllocationProp prop{};
+  CUmemAccessDesc access{};
+  bool async = true;
+  std::thread worker;
+  std::mutex mu;
+  std::condition_variable cv_work, cv_done;
+  std::deque<DrvOp> queue;
+  bool stopping = false;
+  uint64_t next_ticket = 0;                 // submitted
+  std::atomic<uint64_t> done_ticket{0};     // completed
+  std::string drv_error;                    // sticky worker error
+  std::atomic<bool> drv_failed{false};
+  CUevent fence_events[kFenceRing] = {};
+  uint64_t fence_epoch = 0;                 // recorded by the caller
+  uint64_t synced_epoch = 0;                // waited by the worker
+  std::unordered_map<int64_t, CUmemGenericAllocationHandle> phys;  // worker-owned
+  vt_driver_stats dstats{};
+
+  bool is_cuda() const { return ordinal >= 0; }
+  int64_t created_bytes() const {
+    return static_cast<int64_t>(handles.size()) * cfg.chunk_bytes;
+  }
+  int64_t activation_bytes() const {
+    return active_requests * cfg.activation_bytes_per_request;
+  }
+  int64_t free_bytes() const {
+    return cfg.capacity_bytes - cfg.weights_bytes - activation_bytes() - created_bytes();
+  }
+
+  int fail(int code, std::string msg) {
+    last_error = std::move(msg);
+    return code;
+  }
+
+  void log_call(vt_op op, int64_t base, int64_t page, int64_t handle, int64_t pages) {
+    vt_call c{};
+    c.seq = static_cast<int64_t>(log.size());
+    c.op = op;
+    c.base = base;
+    c.page = page;
+    c.handle = handle;
+    c.pages = pages;
+    c.created_bytes_after = created_bytes();
+    log.push_back(c);
+  }
+
+  // ---- worker plumbing ----
+  bool ensure_ctx() {
+    CUcontext cur = nullptr;
+    driver().CtxGetCurrent(&cur);
+    if (cur != ctx) return driver().CtxSetCurrent(ctx) == CUDA_SUCCESS;
+    return true;
+  }
+
+  void submit(DrvOp op) {
+    op.submit_ns = now_ns();
+    op.fence_epoch = fence_epoch;
+    if (!async) {
+      op.ticket = ++next_ticket;
+      execute_run(&op, 1);
+      done_ticket.store(op.ticket);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      op.ticket = ++next_ticket;
+      queue.push_back(op);
+    }
+    cv_work.notify_one();
+  }
+
+  void record_error(const std::string& what) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (drv_error.empty()) drv_error = what;
+    drv_failed.store(true);
+  }
+
+  void wait_fence(uint64_t epoch) {
+    if (epoch == 0 || epoch <= synced_epoch) return;
+    int64_t t0 = now_ns();
+    CUevent ev = fence_events[epoch % kFenceRing];
+    CUresult r = driver().EventSynchronize(ev);
+    if (r != CUDA_SUCCESS) record_error("cuEventSynchronize: " + cu_err(r));
+    synced_epoch = epoch;
+    dstats.fence_waits++;
+    dstats.fence_wait_ns_total += now_ns() - t0;
+  }
+
+  // Executes ops[0..n) which the caller guarantees are in issue order. A run of
+  // maps onto consecutive pages gets one cuMemSetAccess for the whole run.
+  void execute_run(DrvOp* ops, size_t n) {
+    Driver& d = driver();
+    size_t i = 0;
+    while (i < n) {
+      DrvOp& op = ops[i];
+      int64_t t0 = now_ns();
+      switch (op.kind) {
+        case DrvKind::kCreate: {
+          CUmemGenericAllocationHandle h = 0;
+          CUresult r = d.MemCreate(&h, static_cast<size_t>(cfg.chunk_bytes), &prop, 0);
+          if (r != CUDA_SUCCESS) {
+            record_error("cuMemCreate: " + cu_err(r));
+          } else {
+            phys[op.handle_id] = h;
+          }
+          dstats.create_calls++;
+          dstats.create_ns_total += now_ns() - t0;
+          ++i;
+          break;
+        }
+        case DrvKind::kMap: {
+          size_t j = i;
+          CUdeviceptr run_start = op.addr;
+          size_t run_len = 0;
+          while (j < n && ops[j].kind == DrvKind::kMap &&
+                 ops[j].addr == run_start + run_len) {
+            auto it = phys.find(ops[j].handle_id);
+            if (it == phys.end()) {
+              record_error("map of a chunk the driver never created (id " +
+                           std::to_string(ops[j].handle_id) + ")");
+            } else {
+              CUresult r = d.MemMap(ops[j].addr, static_cast<size_t>(cfg.chunk_bytes), 0,
+                                    it->second, 0);
+              if (r != CUDA_SUCCESS) record_error("cuMemMap: " + cu_err(r));
+            }
+            dstats.map_calls++;
+            run_len += static_cast<size_t>(cfg.chunk_bytes);
+            ++j;
+          }
+          CUresult r = d.MemSetAccess(run_start, run_len, &access, 1);
+          if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
+          dstats.access_calls++;
+          dstats.map_ns_total += now_ns() - t0;
+          i = j;
+          break;
+        }
+        case DrvKind::kUnmap: {
+          wait_fence(op.fence_epoch);
+          CUresult r = d.MemUnmap(op.addr, static_cast<size_t>(cfg.chunk_bytes));
+          if (r != CUDA_SUCCESS) record_error("cuMemUnmap: " + cu_err(r));
+          dstats.unmap_calls++;
+          dstats.unmap_ns_total += now_ns() - t0;
+          ++i;
+          break;
+        }
+        case DrvKind::kDestroy: {
+          wait_fence(op.fence_epoch);
+          auto it = phys.find(op.handle_id);
+          if (it != phys.end()) {
+            CUresult r = d.MemRelease(it->second);
+            if (r != CUDA_SUCCESS) record_error("cuMemRelease: " + cu_err(r));
+            phys.erase(it);
+          }
+          dstats.destroy_calls++;
+          dstats.destroy_ns_total += now_ns() - t0;
+          ++i;
+          break;
+        }
+        case DrvKind::kRelease: {
+          wait_fence(op.fence_epoch);
+          CUresult r = d.AddrFree(op.addr, op.size);
+          if (r != CUDA_SUCCESS) record_error("cuMemAddressFree: " + cu_err(r));
+          ++i;
+          break;
+        }
+      }
+    }
+    int64_t lat = now_ns() - ops[n - 1].submit_ns;
+    dstats.max_op_ns = std::max<int64_t>(dstats.max_op_ns, lat);
+    dstats.ops_completed += static_cast<int64_t>(n);
+  }
+
+  void worker_main() {
+    driver().CtxSetCurrent(ctx);
+    std::vector<DrvOp> batch;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_work.wait(lk, [&] { return stopping || !queue.empty(); });
+        if (queue.empty() && stopping) return;
+        batch.assign(queue.begin(), queue.end());
+        queue.clear();
+      }
+      execute_run(batch.data(), batch.size());
+      done_ticket.store(batch.back().ticket);
+      cv_done.notify_all();
+    }
+  }
+};
+
+namespace {
+
+int check_map_args(vt_device* d, int64_t base, int64_t page, int64_t id, RangeState** out) {
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end())
+    return d->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  RangeState& rs = it->second;
+  if (page < 0 || page >= rs.pages)
+    return d->fail(VT_E_INDEX_OUT_OF_RANGE, "page " + std::to_string(page) + " outside range of " +
+                                                std::to_string(rs.pages) + " pages");
+  if (d->handles.find(id) == d->handles.end())
+    return d->fail(VT_E_STALE_HANDLE,
+                   "handle " + std::to_string(id) + " was destroyed or never created");
+  if (rs.slot[static_cast<size_t>(page)] >= 0)
+    return d->fail(VT_E_PAGE_ALREADY_MAPPED,
+                   "page " + std::to_string(page) + " of base " + std::to_string(base) + " is mapped");
+  *out = &rs;
+  return VT_OK;
+}
+
+int do_map(vt_device* d, int64_t base, int64_t page, int64_t id) {
+  RangeState* rs = nullptr;
+  int rc = check_map_args(d, base, page, id, &rs);
+  if (rc) return rc;
+  rs->slot[static_cast<size_t>(page)] = id;
+  rs->mapped++;
+  d->handles[id] += 1;
+  d->mapped_pages++;
+  d->log_call(VT_OP_MAP_PAGE, base, page, id, 0);
+  if (d->is_cuda()) {
+    DrvOp op{};
+    op.kind = DrvKind::kMap;
+    op.handle_id = id;
+    op.addr = rs->va + static_cast<CUdeviceptr>(page) * static_cast<CUdeviceptr>(d->cfg.chunk_bytes);
+    d->submit(op);
+  }
+  return VT_OK;
+}
+
+int do_unmap(vt_device* d, int64_t base, int64_t page, int64_t* id_out) {
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end())
+    return d->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  RangeState& rs = it->second;
+  if (page < 0 || page >= rs.pages || rs.slot[static_cast<size_t>(page)] < 0)
+    return d->fail(VT_E_PAGE_NOT_MAPPED, "page " + std::to_string(page) + " of base " +
+                                             std::to_string(base) + " is not mapped");
+  int64_t id = rs.slot[static_cast<size_t>(page)];
+  rs.slot[static_cast<size_t>(page)] = -1;
+  rs.mapped--;
+  d->handles[id] -= 1;
+  d->mapped_pages--;
+  d->log_call(VT_OP_UNMAP_PAGE, base, page, id, 0);
+  if (d->is_cuda()) {
+    DrvOp op{};
+    op.kind = DrvKind::kUnmap;
+    op.addr = rs.va + static_cast<CUdeviceptr>(page) * static_cast<CUdeviceptr>(d->cfg.chunk_bytes);
+    d->submit(op);
+  }
+  if (id_out) *id_out = id;
+  return VT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
+  if (!cfg || !out) return VT_E_ARG;
+  *out = nullptr;
+  if (cfg->capacity_bytes <= 0 || cfg->chunk_bytes <= 0) return VT_E_ARG;
+  if (cfg->weights_bytes < 0 || cfg->weights_bytes > cfg->capacity_bytes) return VT_E_ARG;
+  vt_device* d = new vt_device();
+  d->cfg = *cfg;
+  d->ordinal = cuda_ordinal;
+  if (cuda_ordinal >= 0) {
+    Driver& drv = driver();
+    if (!drv.loaded) {
+      d->last_error = "CUDA driver unavailable: " + drv.error;
+      static thread_local std::string err;
+      err = d->last_error;
+      std::fprintf(stderr, "vtensor: %s\n", err.c_str());
+      delete d;
+      return VT_E_CUDA;
+    }
+    CUdevice dev;
+    CUresult r = drv.DeviceGet(&dev, cuda_ordinal);
+    if (r == CUDA_SUCCESS) r = drv.PrimaryCtxRetain(&d->ctx, dev);
+    if (r != CUDA_SUCCESS) {
+      std::fprintf(stderr, "vtensor: device %d: %s\n", cuda_ordinal, cu_err(r).c_str());
+      delete d;
+      return VT_E_CUDA;
+    }
+    d->ensure_ctx();
+    d->prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    d->prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    d->prop.location.id = cuda_ordinal;
+    size_t gran = 0;
+    r = drv.Granularity(&gran, &d->prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM);
+    if (r != CUDA_SUCCESS || gran == 0 || cfg->chunk_bytes % static_cast<int64_t>(gran) != 0) {
+      std::fprintf(stderr, "vtensor: chunk %lld is not a multiple of VMM granularity %zu\n",
+                   static_cast<long long>(cfg->chunk_bytes), gran);
+      delete d;
+      return VT_E_ARG;
+    }
+    d->access.location = d->prop.location;
+    d->access.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    for (auto& ev : d->fence_events) {
+      r = drv.EventCreate(&ev, CU_EVENT_DISABLE_TIMING);
+      if (r != CUDA_SUCCESS) {
+        delete d;
+        return VT_E_CUDA;
+      }
+    }
+    d->worker = std::thread([d] { d->worker_main(); });
+  }
+  *out = d;
+  return VT_OK;
+}
+
+int vt_dev_close(vt_device* d) {
+  if (!d) return VT_OK;
+  if (d->is_cuda()) {
+    {
+      std::lock_guard<std::mutex> lk(d->mu);
+      d->stopping = true;
+    }
+    d->cv_work.notify_all();
+    if (d->worker.joinable()) d->worker.join();
+    Driver& drv = driver();
+    d->ensure_ctx();
+    // Tear down whatever the manager left behind (caller is responsible for
+    // having synchronised the streams that read these pages).
+    for (auto& kv : d->ranges) {
+      RangeState& rs = kv.second;
+      for (int64_t p = 0; p < rs.pages; ++p)
+        if (rs.slot[static_cast<size_t>(p)] >= 0)
+          drv.MemUnmap(rs.va + static_cast<CUdeviceptr>(p) * d->cfg.chunk_bytes,
+                       static_cast<size_t>(d->cfg.chunk_bytes));
+      drv.AddrFree(rs.va, static_cast<size_t>(rs.pages * d->cfg.chunk_bytes));
+    }
+    for (auto& kv : d->phys) drv.MemRelease(kv.second);
+    for (auto& ev : d->fence_events)
+      if (ev) drv.EventDestroy(ev);
+  }
+  delete d;
+  return VT_OK;
+}
+
+int vt_dev_is_cuda(const vt_device* d) { return d && d->is_cuda() ? 1 : 0; }
+
+const char* vt_last_error(const vt_device* d) {
+  if (!d) return "null device";
+  return d->last_error.c_str();
+}
+
+// device.py:191-204
+int vt_reserve(vt_device* d, int64_t size, int64_t* base, int64_t* pages) {
+  const int64_t page = d->cfg.chunk_bytes;
+  if (size <= 0 || size % page != 0)
+    return d->fail(VT_E_INVALID_SIZE, "reserve size must be a positive multiple of " +
+                                          std::to_string(page) + ", got " + std::to_string(size));
+  const int64_t n = size / page;
+  RangeState rs;
+  rs.pages = n;
+  rs.slot.assign(static_cast<size_t>(n), -1);
+  if (d->is_cuda()) {
+    d->ensure_ctx();
+    CUdeviceptr va = 0;
+    CUresult r = driver().AddrReserve(&va, static_cast<size_t>(size),
+                                      static_cast<size_t>(page), 0, 0);
+    if (r != CUDA_SUCCESS) return d->fail(VT_E_CUDA, "cuMemAddressReserve: " + cu_err(r));
+    rs.va = va;
+  }
+  const int64_t b = d->next_base;
+  d->next_base += n;  // disjoint ordinal intervals, never reused
+  d->ranges.emplace(b, std::move(rs));
+  d->reserved_bytes += size;
+  d->log_call(VT_OP_RESERVE_ADDRESS, b, 0, 0, n);
+  *base = b;
+  *pages = n;
+  return VT_OK;
+}
+
+// device.py:206-216
+int vt_create_chunk(vt_device* d, int64_t* id) {
+  if (d->free_bytes() < d->cfg.chunk_bytes)
+    return d->fail(VT_E_OUT_OF_MEMORY, "need " + std::to_string(d->cfg.chunk_bytes) + " bytes, " +
+                                           std::to_string(d->free_bytes()) + " free");
+  const int64_t h = d->next_handle++;
+  d->handles.emplace(h, 0);
+  d->log_call(VT_OP_CREATE_CHUNK, 0, 0, h, 0);
+  if (d->is_cuda()) {
+    DrvOp op{};
+    op.kind = DrvKind::kCreate;
+    op.handle_id = h;
+    d->submit(op);
+  }
+  *id = h;
+  return VT_OK;
+}
+
+// device.py:218-233
+int vt_map_page(vt_device* d, int64_t base, int64_t page, int64_t id) {
+  return do_map(d, base, page, id);
+}
+
+int vt_map_pages(vt_device* d, int64_t base, int64_t first_page, const int64_t* ids, int64_t n,
+                 int64_t* n_done) {
+  int64_t k = 0;
+  int rc = VT_OK;
+  for (; k < n; ++k) {
+    rc = do_map(d, base, first_page + k, ids[k]);
+    if (rc) break;
+  }
+  if (n_done) *n_done = k;
+  return rc;
+}
+
+// device.py:235-245
+int vt_unmap_page(vt_device* d, int64_t base, int64_t page, int64_t* id) {
+  return do_unmap(d, base, page, id);
+}
+
+int vt_unmap_tail(vt_device* d, int64_t base, int64_t from_page, int64_t down_to, int64_t* ids,
+                  int64_t* n_done) {
+  int64_t k = 0;
+  int rc = VT_OK;
+  for (int64_t p = from_page; p >= down_to; --p, ++k) {
+    rc = do_unmap(d, base, p, ids ? &ids[k] : nullptr);
+    if (rc) break;
+  }
+  if (n_done) *n_done = k;
+  return rc;
+}
+
+// device.py:247-257
+int vt_release(vt_device* d, int64_t base) {
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end())
+    return d->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  if (it->second.mapped)
+    return d->fail(VT_E_RANGE_STILL_MAPPED, "range base " + std::to_string(base) + " still has " +
+                                               std::to_string(it->second.mapped) + " mapped pages");
+  if (d->is_cuda()) {
+    DrvOp op{};
+    op.kind = DrvKind::kRelease;
+    op.addr = it->second.va;
+    op.size = static_cast<size_t>(it->second.pages * d->cfg.chunk_bytes);
+    d->submit(op);
+  }
+  d->reserved_bytes -= it->second.pages * d->cfg.chunk_bytes;
+  d->ranges.erase(it);
+  d->log_call(VT_OP_RELEASE_ADDRESS, base, 0, 0, 0);
+  return VT_OK;
+}
+
+// device.py:259-268
+int vt_destroy_chunk(vt_device* d, int64_t id) {
+  auto it = d->handles.find(id);
+  if (it == d->handles.end())
+    return d->fail(VT_E_STALE_HANDLE,
+                   "handle " + std::to_string(id) + " was destroyed or never created");
+  if (it->second != 0)
+    return d->fail(VT_E_CHUNK_STILL_MAPPED, "handle " + std::to_string(id) + " still mapped " +
+                                                std::to_string(it->second) + " times");
+  d->handles.erase(it);
+  d->log_call(VT_OP_DESTROY_CHUNK, 0, 0, id, 0);
+  if (d->is_cuda()) {
+    DrvOp op{};
+    op.kind = DrvKind::kDestroy;
+    op.handle_id = id;
+    d->submit(op);
+  }
+  return VT_OK;
+}
+
+// device.py:166-174
+int vt_set_active_requests(vt_device* d, int64_t n) {
+  if (n < 0) return d->fail(VT_E_ARG, "active request count cannot be negative");
+  const int64_t delta = (n - d->active_requests) * d->cfg.activation_bytes_per_request;
+  if (delta > d->free_bytes())
+    return d->fail(VT_E_OUT_OF_MEMORY,
+                   "activation scratch for " + std::to_string(n) + " requests exceeds free memory");
+  d->active_requests = n;
+  return VT_OK;
+}
+
+int vt_get_stats(const vt_device* d, vt_stats* s) {
+  s->created_bytes = d->created_bytes();
+  s->reserved_virtual_bytes = d->reserved_bytes;
+  s->mapped_page_count = d->mapped_pages;
+  s->free_bytes = d->free_bytes();
+  s->activation_bytes = d->activation_bytes();
+  s->active_requests = d->active_requests;
+  s->live_handles = static_cast<int64_t>(d->handles.size());
+  s->live_ranges = static_cast<int64_t>(d->ranges.size());
+  return VT_OK;
+}
+
+// device.py:272-283
+int vt_resolve(const vt_device* d, int64_t base, int64_t page, int64_t* id) {
+  auto* md = const_cast<vt_device*>(d);
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end())
+    return md->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  const RangeState& rs = it->second;
+  if (page < 0 || page >= rs.pages)
+    return md->fail(VT_E_INDEX_OUT_OF_RANGE, "page " + std::to_string(page) +
+                                                 " outside range of " + std::to_string(rs.pages) +
+                                                 " pages");
+  if (rs.slot[static_cast<size_t>(page)] < 0)
+    return md->fail(VT_E_PAGE_NOT_MAPPED, "page " + std::to_string(page) + " of base " +
+                                              std::to_string(base) + " is not mapped");
+  *id = rs.slot[static_cast<size_t>(page)];
+  return VT_OK;
+}
+
+int vt_handle_alive(const vt_device* d, int64_t id, int64_t* map_count) {
+  auto it = d->handles.find(id);
+  if (it == d->handles.end()) return VT_E_STALE_HANDLE;
+  if (map_count) *map_count = it->second;
+  return VT_OK;
+}
+
+int vt_live_handles(const vt_device* d, int64_t* ids, int64_t cap, int64_t* n) {
+  int64_t k = 0;
+  for (const auto& kv : d->handles) {
+    if (k < cap) ids[k] = kv.first;
+    ++k;
+  }
+  *n = k;
+  return k <= cap ? VT_OK : VT_E_ARG;
+}
+
+int vt_live_ranges(const vt_device* d, int64_t* bases, int64_t* pages, int64_t cap, int64_t* n) {
+  int64_t k = 0;
+  for (const auto& kv : d->ranges) {
+    if (k < cap) {
+      bases[k] = kv.first;
+      pages[k] = kv.second.pages;
+    }
+    ++k;
+  }
+  *n = k;
+  return k <= cap ? VT_OK : VT_E_ARG;
+}
+
+// device.py:291-295
+int vt_range_mappings(const vt_device* d, int64_t base, int64_t* pages_out, int64_t* ids_out,
+                      int64_t cap, int64_t* n) {
+  auto* md = const_cast<vt_device*>(d);
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end())
+    return md->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  int64_t k = 0;
+  const RangeState& rs = it->second;
+  for (int64_t p = 0; p < rs.pages; ++p) {
+    if (rs.slot[static_cast<size_t>(p)] < 0) continue;
+    if (k < cap) {
+      pages_out[k] = p;
+      ids_out[k] = rs.slot[static_cast<size_t>(p)];
+    }
+    ++k;
+  }
+  *n = k;
+  return k <= cap ? VT_OK : VT_E_ARG;
+}
+
+int64_t vt_call_log_len(const vt_device* d) { return static_cast<int64_t>(d->log.size()); }
+
+int vt_call_log_read(const vt_device* d, int64_t from, vt_call* buf, int64_t cap, int64_t* n) {
+  const int64_t total = static_cast<int64_t>(d->log.size());
+  if (from < 0) from = 0;
+  int64_t k = std::max<int64_t>(0, std::min<int64_t>(cap, total - from));
+  if (k) std::memcpy(buf, d->log.data() + from, static_cast<size_t>(k) * sizeof(vt_call));
+  *n = k;
+  return VT_OK;
+}
+
+uint64_t vt_ticket(const vt_device* d) {
+  auto* md = const_cast<vt_device*>(d);
+  std::lock_guard<std::mutex> lk(md->mu);
+  return d->next_ticket;
+}
+
+int vt_wait(vt_device* d, uint64_t ticket) {
+  if (!d->is_cuda()) return VT_OK;
+  if (d->done_ticket.load() < ticket) {
+    std::unique_lock<std::mutex> lk(d->mu);
+    d->cv_done.wait(lk, [&] { return d->done_ticket.load() >= ticket || d->drv_failed.load(); });
+  }
+  if (d->drv_failed.load()) {
+    std::lock_guard<std::mutex> lk(d->mu);
+    return d->fail(VT_E_CUDA, d->drv_error);
+  }
+  return VT_OK;
+}
+
+int vt_poll(const vt_device* d, uint64_t ticket, int* done) {
+  *done = (!d->is_cuda() || d->done_ticket.load() >= ticket) ? 1 : 0;
+  return d->drv_failed.load() ? VT_E_CUDA : VT_OK;
+}
+
+int vt_fence(vt_device* d, void* stream) {
+  if (!d->is_cuda()) return VT_OK;
+  d->ensure_ctx();
+  // Worker may still need the slot we are about to overwrite; re-recording is
+  // safe (the later event completes no earlier than the old one).
+  uint64_t e = d->fence_epoch + 1;
+  CUresult r = driver().EventRecord(d->fence_events[e % kFenceRing],
+                                    reinterpret_cast<CUstream>(stream));
+  if (r != CUDA_SUCCESS) return d->fail(VT_E_CUDA, "cuEventRecord: " + cu_err(r));
+  std::lock_guard<std::mutex> lk(d->mu);
+  d->fence_epoch = e;
+  return VT_OK;
+}
+
+int vt_set_async(vt_device* d, int enabled) {
+  if (!d->is_cuda()) return VT_OK;
+  if (!enabled) vt_wait(d, vt_ticket(d));  // drain before switching to inline
+  d->async = enabled != 0;
+  return VT_OK;
+}
+
+int vt_driver_stats_get(const vt_device* d, vt_driver_stats* out) {
+  *out = d->dstats;
+  return VT_OK;
+}
+
+int vt_va(const vt_device* d, int64_t base, uint64_t* devptr) {
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end()) {
+    auto* md = const_cast<vt_device*>(d);
+    return md->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  }
+  *devptr = static_cast<uint64_t>(it->second.va);
+  return VT_OK;
+}
+
+int vt_encode_tensor_map(const vt_device* d, uint64_t global_addr, int rank, const uint64_t* dims,
+                         const uint64_t* strides_bytes, const uint32_t* box, int swizzle_128b,
+                         void* out128) {
+  (void)d;
+  Driver& drv = driver();
+  if (!drv.loaded) return VT_E_CUDA;
+  cuuint32_t estride[5] = {1, 1, 1, 1, 1};
+  CUresult r = drv.TensorMapEncodeTiled(
+      reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+      static_cast<cuuint32_t>(rank), reinterpret_cast<void*>(global_addr),
+      reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides_bytes),
+      reinterpret_cast<const cuuint32_t*>(box), estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      swizzle_128b ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? VT_OK : VT_E_CUDA;
+}
+
+}  // extern "C"
