@@ -1,0 +1,527 @@
+#!/usr/bin/env python
+"""bench.py — vTensor decode step on B200 (BASELINE.json config 2 by default).
+
+One *step* = one decode step of a Llama-3-8B-shaped batch (32 q / 8 kv heads,
+d 128, bf16, 32 layers, batch 64 per GPU, ~4k context) through the product path:
+
+  host : vTensor extend for the NEXT token of every request (VTS.extend ->
+         VTO.p_alloc/map_chunks -> libvtensor; cuMemCreate/cuMemMap/
+         cuMemSetAccess run on the shim's worker thread, overlapping the GPU
+         work already queued), wait(ticket) before the launch that writes the
+         new pages, append_token bookkeeping;
+  GPU  : vt_kv_append (new K/V of all 32 layers) + 32 x vt_decode_attention
+         (split-KV kernel + LSE combine).
+
+Context lengths are staggered (4081..4096 at start) so that every step some
+requests cross a 16-token chunk boundary and need a real 2 MiB chunk mapped.
+
+Metric (BASELINE.json): decode-attn KV GB/s = algorithmic bytes
+(KV read + q read + out write + appended K/V) / time; tokens/s and the extend
+latency are reported beside it. ``value`` is device-timed with inputs resident
+in HBM (KV working set 32 GiB >> 126 MB L2, so no flush is needed); ``e2e``
+repeats the run through the public API with q / new-K/V copied from pinned host
+memory and the outputs copied back inside the timed region.
+
+Multi-GPU (torchrun, one process per GPU): requests are partitioned — each GPU
+owns its own VMM chunk pool and its own 64 requests (weak scaling); there is no
+collective on the data path, only a barrier and a max-over-ranks of the timings.
+
+``--impl reference`` times the reference arm: the CPU fp32 restatement of the
+same attention (oracle/attention_ref.py, the only CPU implementation of this
+path — the reference package has none) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+MIB = 1 << 20
+GIB = 1 << 30
+
+CONFIGS = {
+    # name: (layers, kv_heads, q_heads, batch_per_gpu, ctx)
+    "llama3-8b-decode": (32, 8, 32, 64, 4096),
+    "toy-cfg1": (1, 8, 8, 8, 4096),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(CONFIGS), default="llama3-8b-decode")
+    ap.add_argument("--split", type=int, default=0, help="split-KV tokens per CTA (0=auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="run N untimed steps only (for ncu), print nothing")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self) -> None:
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[4:8])
+                          if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ dist plumbing --
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------- the workload --
+class DecodeWorkload:
+    """64 requests of one GPU, their vTensor spaces, and the per-step driver."""
+
+    def __init__(self, cfg_name: str, split: int, seed: int):
+        import torch
+
+        import paper_2407_15309_b200 as vt
+        from paper_2407_15309_b200.attention import DecodeWorkspace
+        from paper_2407_15309_b200.kv_layout import KVGeometry, chunk_view
+
+        L, hkv, hq, B, ctx = CONFIGS[cfg_name]
+        self.L, self.hkv, self.hq, self.B, self.ctx = L, hkv, hq, B, ctx
+        self.max_seq = ctx + 1024
+        self.cfg = vt.SimConfig(
+            capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB, weights_bytes=0,
+            geometry=vt.ModelGeometry(layers=L, kv_heads=hkv, head_dim=128, elem_bytes=2),
+            max_seq_len=self.max_seq, initial_alloc_tokens=0, lookahead_chunks=1, max_batch=B)
+        self.dev = vt.VirtualMemoryDevice(
+            vt.DeviceConfig(capacity_bytes=self.cfg.capacity_bytes,
+                            chunk_size_bytes=self.cfg.chunk_size_bytes),
+            cuda_ordinal=torch.cuda.current_device())
+        self.pool = vt.TensorPool(self.cfg.tokens_per_chunk)
+        self.ops = vt.VTensorOps(self.dev, self.pool, self.cfg)
+        self.sched = vt.VTensorScheduler(self.ops)
+        self.geo = KVGeometry.from_config(self.cfg, hq)
+        tpc = self.cfg.tokens_per_chunk
+        self.rids = [f"r{b}" for b in range(B)]
+        # staggered lengths: ctx-15 .. ctx so chunk boundaries are crossed every step
+        self.lens = [ctx - (tpc - 1) + (b % tpc) if ctx >= tpc else ctx for b in range(B)]
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        vas = []
+        for rid, n in zip(self.rids, self.lens):
+            self.sched.create(rid, [1] * n)
+            self.sched.mark_prefilled(rid)
+            vas.append(self.dev.va(self.sched.mem[rid].vt.space.rng))
+        self.dev.wait()
+        for va, rid in zip(vas, self.rids):
+            pages = self.sched.mem[rid].vt.space.mapped_pages
+            view = chunk_view(va, pages, self.geo)
+            view.copy_(torch.randn(view.shape, generator=gen, device="cuda").to(torch.bfloat16))
+        self.kv_va = torch.tensor(vas, dtype=torch.int64, device="cuda")
+        self.seq = torch.tensor(self.lens, dtype=torch.int32, device="cuda")
+        self.q = torch.randn(L, B, hq, 128, generator=gen, device="cuda").to(torch.bfloat16)
+        self.k_new = torch.randn(L, B, hkv, 128, generator=gen, device="cuda").to(torch.bfloat16)
+        self.v_new = torch.randn_like(self.k_new)
+        self.out = torch.empty_like(self.q)
+        self.split = split
+        self.ws = DecodeWorkspace(self.geo, B, self.max_seq, split)
+        self.stream = torch.cuda.current_stream()
+        self.host_lens = list(self.lens)
+        self.stalls = 0
+        self.extend_ns: list[int] = []
+        self.chunks_mapped = 0
+        self._issue_extends()  # capacity for the first step's token
+        torch.cuda.synchronize()
+
+    # -- manager half ---------------------------------------------------------
+    def _issue_extends(self):
+        t0 = time.perf_counter_ns()
+        n = 0
+        for rid, length in zip(self.rids, self.host_lens):
+            n += self.sched.extend(rid, length + 1)
+        if n:
+            self.extend_ns.append((time.perf_counter_ns() - t0) // n)
+        self.chunks_mapped += n
+
+    def algorithmic_bytes_per_step(self) -> int:
+        """KV read (all layers, len+1 tokens incl. the new one) + q + out + appended K/V."""
+        kv = sum(2 * (n + 1) * self.hkv * 128 * 2 for n in self.host_lens) * self.L
+        qo = 2 * self.q.numel() * 2
+        app = 2 * self.k_new.numel() * 2
+        return kv + qo + app
+
+    def decode_bytes_per_launch(self) -> int:
+        return (sum(2 * (n + 1) * self.hkv * 128 * 2 for n in self.host_lens)
+                + 2 * self.B * self.hq * 128 * 2)
+
+    # -- one step -------------------------------------------------------------
+    def step(self, q=None, k_new=None, v_new=None, out=None, layer_events=None):
+        from paper_2407_15309_b200.attention import decode_attention, kv_append
+
+        q = self.q if q is None else q
+        k_new = self.k_new if k_new is None else k_new
+        v_new = self.v_new if v_new is None else v_new
+        out = self.out if out is None else out
+        ticket = self.dev.ticket()
+        if not self.dev.ready(ticket):
+            self.stalls += 1  # mapping not done when the launch was due
+        self.dev.wait(ticket)
+        kv_append(k_new, v_new, self.kv_va, self.seq, self.geo)
+        self.seq.add_(1)
+        mx = max(self.host_lens) + 1
+        launches = 1
+        for layer in range(self.L):
+            if layer_events is not None:
+                layer_events[layer][0].record(self.stream)
+            decode_attention(q[layer], self.kv_va, self.seq, layer, self.geo, mx,
+                             out=out[layer], workspace=self.ws, split_tokens=self.split)
+            if layer_events is not None:
+                layer_events[layer][1].record(self.stream)
+            launches += 2 if math.ceil(mx / (self.split or 512)) > 1 else 1
+        self.dev.fence(self.stream.cuda_stream)
+        for rid in self.rids:
+            self.sched.append_token(rid, 1)
+        self.host_lens = [n + 1 for n in self.host_lens]
+        self._issue_extends()  # next step's pages: overlap with this step's kernels
+        return launches
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    wl = DecodeWorkload(args.config, args.split, seed=1234 + rank)
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            wl.step()
+        torch.cuda.synchronize()
+        return
+    for _ in range(args.warmup):
+        wl.step()
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # ---- device-resident timed region ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(wl.L)]
+    layer_ms = []
+    bytes_total = 0
+    decode_bytes = 0
+    launches = 0
+    stalls0 = wl.stalls
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier(world)
+        start.record()
+        for _ in range(args.steps):
+            bytes_total += wl.algorithmic_bytes_per_step()
+            decode_bytes += wl.decode_bytes_per_launch() * wl.L
+            launches += wl.step(layer_events=ev)
+            layer_ms.append(ev)  # per-launch decode durations (events on the launch stream)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(wl.L)]
+        stop.record()
+        torch.cuda.synchronize()
+    elapsed_ms = start.elapsed_time(stop)
+    kern_ms = sum(a.elapsed_time(b) for evs in layer_ms for a, b in evs)
+    n_decode = args.steps * wl.L
+    stalls = wl.stalls - stalls0
+    elapsed_max = max_over_ranks(elapsed_ms, world)
+    bytes_all = sum_over_ranks(bytes_total, world)
+    tokens_all = wl.B * args.steps * world
+    value = bytes_all / (elapsed_max * 1e-3) / 1e9
+
+    # ---- e2e: host buffers through the public API ----
+    e2e = None
+    if not args.no_e2e:
+        host_q = torch.empty(wl.q.shape, dtype=torch.bfloat16, pin_memory=True).copy_(wl.q)
+        host_k = torch.empty(wl.k_new.shape, dtype=torch.bfloat16, pin_memory=True).copy_(wl.k_new)
+        host_v = torch.empty(wl.v_new.shape, dtype=torch.bfloat16, pin_memory=True).copy_(wl.v_new)
+        host_o = torch.empty(wl.out.shape, dtype=torch.bfloat16, pin_memory=True)
+        dq, dk, dv = torch.empty_like(wl.q), torch.empty_like(wl.k_new), torch.empty_like(wl.v_new)
+        e_bytes = 0
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e_bytes += wl.algorithmic_bytes_per_step()
+            dq.copy_(host_q, non_blocking=True)
+            dk.copy_(host_k, non_blocking=True)
+            dv.copy_(host_v, non_blocking=True)
+            wl.step(q=dq, k_new=dk, v_new=dv)
+            host_o.copy_(wl.out, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+        e_all = sum_over_ranks(e_bytes, world)
+        e2e = {"value": round(e_all / (e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "tokens_per_s": round(wl.B * args.steps * world / (e_ms * 1e-3), 1),
+               "ms_per_step": round(e_ms / args.steps, 4),
+               "h2d_bytes_per_step": int((host_q.numel() + host_k.numel() + host_v.numel()) * 2),
+               "d2h_bytes_per_step": int(host_o.numel() * 2)}
+
+    drv = wl.dev.driver_stats()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    per_launch_s = kern_ms * 1e-3 / n_decode
+    achieved = (decode_bytes / n_decode) / per_launch_s / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(REPO, "profiles", "decode_traffic.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, budget_s=8.0)
+
+    if rank == 0:
+        ext = sorted(wl.extend_ns) or [0]
+        line = {
+            "metric": "decode-attn KV GB/s (% of HBM peak) and tokens/s; vTensor extend latency",
+            "value": round(value, 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(elapsed_max / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (seeded randn bf16 KV in real cuMemMap'd 2 MiB chunks)",
+            "config": {
+                "workload": f"{args.config}: decode step, {wl.L} layers, {wl.hq} q / {wl.hkv} kv "
+                            f"heads, d 128, batch {wl.B}/GPU, ctx {min(wl.lens)}..{max(wl.lens)}",
+                "batch_per_gpu": wl.B, "context": wl.ctx, "layers": wl.L,
+                "parallelism": f"request-partition x{world} (no collective)",
+                "l2": "inputs larger than L2 (KV working set %.1f GiB)" % (
+                    sum(wl.host_lens) * wl.cfg.bytes_per_token / GIB),
+                "split_tokens": args.split or 512,
+            },
+            "tokens_per_s": round(tokens_all / (elapsed_max * 1e-3), 1),
+            "hbm_frac_of_step": round(value / hbm_peak, 4),
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "vt::decode_splitkv_kernel<4>",
+                "achieved": round(achieved, 1),
+                "peak": hbm_peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4),
+                "traffic": traffic,
+                "per_launch_us": round(per_launch_s * 1e6, 2),
+                "algorithmic_bytes_per_launch": int(decode_bytes / n_decode),
+            },
+            "extend": {
+                "chunks_mapped": wl.chunks_mapped,
+                "host_submit_us_p50": round(ext[len(ext) // 2] / 1e3, 2),
+                "host_submit_us_p99": round(ext[min(len(ext) - 1, int(len(ext) * 0.99))] / 1e3, 2),
+                "driver_map_us_mean": round(drv["map_ns_total"] / max(drv["map_calls"], 1) / 1e3, 2),
+                "driver_create_us_mean": round(drv["create_ns_total"] / max(drv["create_calls"], 1) / 1e3, 2),
+                "stalled_steps": stalls,
+                "hidden": stalls == 0,
+            },
+            "gpu_launches": launches + 0,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+    wl.dev.wait()
+    torch.cuda.synchronize()
+
+
+# --------------------------------------------------------- CPU / reference --
+def cpu_baseline(cfg_name: str, budget_s: float = 8.0) -> dict:
+    """The oracle's fp32 attention on the host cores over a bounded sample of
+    the same workload (a few requests of one layer), GB/s of bf16 KV bytes."""
+    import torch
+
+    from oracle.attention_ref import decode_attention_torch_cpu
+
+    L, hkv, hq, B, ctx = CONFIGS[cfg_name]
+    threads = torch.get_num_threads()
+    gen = torch.Generator().manual_seed(0)
+    nb = min(B, 8)
+    k = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
+    v = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
+    q = torch.randn(nb, hq, 128, generator=gen).to(torch.bfloat16)
+    lens = [ctx] * nb
+    decode_attention_torch_cpu(q, k, v, lens)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < budget_s and reps < 200:
+        decode_attention_torch_cpu(q, k, v, lens)
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    kv_bytes = 2 * nb * hkv * ctx * 128 * 2 + 2 * nb * hq * 128 * 2
+    cpu_name = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu_name = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"value": round(kv_bytes / dt / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{nb} requests x 1 layer x {ctx} tokens ({hq}q/{hkv}kv heads), {reps} reps",
+            "tokens_per_s_equiv": round(nb / (dt * L), 2),
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_name}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import torch
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    L, hkv, hq, B, ctx = CONFIGS[args.config]
+    from oracle.attention_ref import decode_attention_torch_cpu
+
+    gen = torch.Generator().manual_seed(0)
+    nb = min(B, 4)
+    k = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
+    v = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
+    q = torch.randn(nb, hq, 128, generator=gen).to(torch.bfloat16)
+    lens = [ctx] * nb
+    for _ in range(args.warmup):
+        decode_attention_torch_cpu(q, k, v, lens)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        decode_attention_torch_cpu(q, k, v, lens)
+    dt = time.perf_counter() - t0
+    kv_bytes = (2 * nb * hkv * ctx * 128 * 2 + 2 * nb * hq * 128 * 2) * args.steps
+    value = kv_bytes / dt / 1e9
+    sample = f"{nb} requests x 1 layer x {ctx} tokens per step ({hq}q/{hkv}kv heads)"
+    line = {
+        "impl": "reference",
+        "metric": "decode-attn KV GB/s (% of HBM peak) and tokens/s; vTensor extend latency",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s",
+                         "cores": torch.get_num_threads(), "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, world, rank)
+        return
+    world, rank, local = dist_setup(args)
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

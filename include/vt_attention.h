@@ -1,0 +1,78 @@
+/*
+ * vt_attention.h — C ABI of libvtattn.so: attention over a vTensor KV cache.
+ *
+ * The reference (kvsim) has no attention: its compute slot is the cost
+ * formula at engine.py:499-511 (`prefill_cost_per_token * prefill_tokens +
+ * decode_cost_per_request * batch`). These entry points are what that slot
+ * calls instead (SURVEY.md §8(b) seam 2): decode over the batch, prefill /
+ * prefix-prefill for admitted requests, and the KV append of new tokens.
+ *
+ * KV layout (kv_layout.py): every request owns one contiguous VA reserved for
+ * max_seq_len (vt_reserve); chunk c of that VA (vt_map_page) holds tokens
+ * [c*tpc, (c+1)*tpc) of ALL layers (config.py:48-50, 86-88). Inside a chunk,
+ * block (layer, K|V, kv_head) is a dense [tpc][head_dim] bf16 tile at byte
+ * offset ((layer*2 + kv)*kv_heads + head) * tpc*head_dim*2. Kernels address
+ * K/V by arithmetic off the request's VA — there is no block table.
+ *
+ * All pointers are device pointers unless stated; every call is asynchronous
+ * on `stream` (a cudaStream_t) and returns 0 or a cudaError_t value.
+ */
+#ifndef VT_ATTENTION_H_
+#define VT_ATTENTION_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vt_kv_geometry {
+  int32_t layers;           /* ModelGeometry.layers (config.py:42) */
+  int32_t kv_heads;         /* ModelGeometry.kv_heads (config.py:43) */
+  int32_t head_dim;         /* ModelGeometry.head_dim, must be 128 */
+  int32_t q_heads;          /* query heads; q_heads / kv_heads = GQA group */
+  int32_t tokens_per_chunk; /* SimConfig.tokens_per_chunk (config.py:86-88) */
+  int32_t _pad;
+  int64_t chunk_bytes;      /* SimConfig.chunk_size_bytes (2 MiB) */
+} vt_kv_geometry;
+
+/* Decode attention for one layer (row a27): for each request b and q head h,
+ * out[b,h,:] = softmax(scale * q[b,h,:] . K[b, 0:len_b, h/G]^T) V[b, 0:len_b, h/G].
+ *   q, out   : [batch, q_heads, head_dim] bf16
+ *   kv_va    : [batch] u64 request VAs;  seq_lens : [batch] i32
+ *   max_seq_len: host upper bound of seq_lens (sizes the split grid)
+ *   workspace: >= vt_decode_workspace_bytes(...) bytes (fp32 split partials)
+ *   split_tokens: KV tokens per CTA work unit (multiple of 64), 0 = default */
+int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
+                        const uint64_t* kv_va, const int32_t* seq_lens, int32_t batch,
+                        int32_t max_seq_len, float scale, void* out, void* workspace,
+                        size_t workspace_bytes, int32_t split_tokens, void* stream);
+size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t batch, int32_t max_seq_len,
+                                 int32_t split_tokens);
+
+/* KV append (row a29): write the K/V of one new token per request at token
+ * position positions[b], for layers [layer_begin, layer_begin + n_layers).
+ *   k_new, v_new : [n_layers, batch, kv_heads, head_dim] bf16 */
+int vt_kv_append(const vt_kv_geometry* g, int32_t layer_begin, int32_t n_layers,
+                 const void* k_new, const void* v_new, const uint64_t* kv_va,
+                 const int32_t* positions, int32_t batch, void* stream);
+
+/* Prefill / prefix-prefill (row a28): n_new query tokens per request at
+ * positions [start_b, start_b + n_new) attend causally to KV [0, start_b + i]
+ * already in the cache (prefix chunks shared through the rTree are mapped into
+ * the request's own VA, so they are read in place).
+ *   q   : [batch, n_new, q_heads, head_dim] bf16;  out : same shape
+ *   start: [batch] i32 (shared prefix length, multiple of 128 for the tcgen05 path) */
+int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
+                         const uint64_t* kv_va, const int32_t* start, int32_t batch,
+                         int32_t n_new, float scale, void* out, void* stream);
+
+/* Number of kernel launches the last call on this thread issued (bench
+ * accounting of "gpu_launches"). */
+int32_t vt_attn_last_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VT_ATTENTION_H_ */

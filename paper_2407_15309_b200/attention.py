@@ -1,0 +1,150 @@
+"""Attention over a vTensor KV cache (rows a27-a29) — calls into libvtattn.so.
+
+These functions are the compute slot the reference leaves as a cost formula
+(kvsim/engine.py:499-511). Every tensor must already be on the GPU; there is
+no CPU or eager-PyTorch fallback — a missing library or a CPU tensor raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from ctypes import POINTER, c_float, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+
+import torch
+
+from ._native import _load
+from .kv_layout import KVGeometry
+
+
+class _Geo(ctypes.Structure):
+    _fields_ = [
+        ("layers", c_int32),
+        ("kv_heads", c_int32),
+        ("head_dim", c_int32),
+        ("q_heads", c_int32),
+        ("tokens_per_chunk", c_int32),
+        ("_pad", c_int32),
+        ("chunk_bytes", c_int64),
+    ]
+
+
+_lib = None
+
+
+def attn_lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        lib = _load("libvtattn.so")
+        P = c_void_p
+        lib.vt_decode_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, c_int32,
+                                            c_float, P, P, c_size_t, c_int32, P]
+        lib.vt_decode_attention.restype = c_int
+        lib.vt_decode_workspace_bytes.argtypes = [POINTER(_Geo), c_int32, c_int32, c_int32]
+        lib.vt_decode_workspace_bytes.restype = c_size_t
+        lib.vt_kv_append.argtypes = [POINTER(_Geo), c_int32, c_int32, P, P, P, P, c_int32, P]
+        lib.vt_kv_append.restype = c_int
+        lib.vt_prefill_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, c_int32,
+                                             c_float, P, P]
+        lib.vt_prefill_attention.restype = c_int
+        lib.vt_attn_last_launches.argtypes = []
+        lib.vt_attn_last_launches.restype = c_int32
+        _lib = lib
+    return _lib
+
+
+ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_workspace_bytes", "vt_kv_append",
+                "vt_prefill_attention", "vt_attn_last_launches")
+
+
+def _geo(g: KVGeometry) -> _Geo:
+    return _Geo(g.layers, g.kv_heads, g.head_dim, g.q_heads, g.tokens_per_chunk, 0, g.chunk_bytes)
+
+
+def _need_cuda(*tensors: torch.Tensor) -> None:
+    for t in tensors:
+        if not t.is_cuda:
+            raise RuntimeError("vTensor attention runs on the GPU only; got a CPU tensor")
+        if not t.is_contiguous():
+            raise RuntimeError("vTensor attention needs contiguous tensors")
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise RuntimeError(f"{what} failed: cudaError {rc}")
+
+
+def _stream(stream: torch.cuda.Stream | None) -> int:
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+class DecodeWorkspace:
+    """Split-KV partials buffer sized for (batch, max_seq_len)."""
+
+    def __init__(self, geo: KVGeometry, batch: int, max_seq_len: int, split_tokens: int = 0,
+                 device: str = "cuda") -> None:
+        self.geo, self.split_tokens = geo, split_tokens
+        nbytes = attn_lib().vt_decode_workspace_bytes(ctypes.byref(_geo(geo)), batch,
+                                                       max_seq_len, split_tokens)
+        self.buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        self.batch, self.max_seq_len = batch, max_seq_len
+
+
+def decode_attention(q: torch.Tensor, kv_va: torch.Tensor, seq_lens: torch.Tensor, layer: int,
+                     geo: KVGeometry, max_seq_len: int, out: torch.Tensor | None = None,
+                     workspace: DecodeWorkspace | None = None, scale: float | None = None,
+                     split_tokens: int = 0, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """q ``[B, Hq, d]`` bf16 -> out ``[B, Hq, d]`` bf16 for one layer.
+
+    ``kv_va`` is an int64 CUDA tensor of request VAs (``device.va(space.rng)``),
+    ``seq_lens`` an int32 CUDA tensor; ``max_seq_len`` a host bound on it."""
+    B = q.shape[0]
+    if q.dtype != torch.bfloat16 or q.shape[1:] != (geo.q_heads, geo.head_dim):
+        raise ValueError(f"q must be bf16 [B, {geo.q_heads}, {geo.head_dim}]")
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None or workspace.batch < B or workspace.max_seq_len < max_seq_len:
+        workspace = DecodeWorkspace(geo, B, max_seq_len, split_tokens)
+    _need_cuda(q, kv_va, seq_lens, out)
+    if scale is None:
+        scale = 1.0 / math.sqrt(geo.head_dim)
+    rc = attn_lib().vt_decode_attention(
+        ctypes.byref(_geo(geo)), layer, q.data_ptr(), kv_va.data_ptr(), seq_lens.data_ptr(), B,
+        max_seq_len, scale, out.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(),
+        workspace.split_tokens or split_tokens, _stream(stream))
+    _check(rc, "vt_decode_attention")
+    return out
+
+
+def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, kv_va: torch.Tensor,
+              positions: torch.Tensor, geo: KVGeometry, layer_begin: int = 0,
+              stream: torch.cuda.Stream | None = None) -> None:
+    """Write ``[n_layers, B, Hkv, d]`` new-token K/V at ``positions[b]``."""
+    _need_cuda(k_new, v_new, kv_va, positions)
+    n_layers, B = k_new.shape[0], k_new.shape[1]
+    rc = attn_lib().vt_kv_append(ctypes.byref(_geo(geo)), layer_begin, n_layers, k_new.data_ptr(),
+                                 v_new.data_ptr(), kv_va.data_ptr(), positions.data_ptr(), B,
+                                 _stream(stream))
+    _check(rc, "vt_kv_append")
+
+
+def prefill_attention(q: torch.Tensor, kv_va: torch.Tensor, start: torch.Tensor, layer: int,
+                      geo: KVGeometry, out: torch.Tensor | None = None, scale: float | None = None,
+                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """q ``[B, n_new, Hq, d]``: new tokens at ``[start_b, start_b + n_new)``
+    attend causally to the KV already in the cache (shared prefix included)."""
+    B, n_new = q.shape[0], q.shape[1]
+    if out is None:
+        out = torch.empty_like(q)
+    _need_cuda(q, kv_va, start, out)
+    if scale is None:
+        scale = 1.0 / math.sqrt(geo.head_dim)
+    rc = attn_lib().vt_prefill_attention(ctypes.byref(_geo(geo)), layer, q.data_ptr(),
+                                         kv_va.data_ptr(), start.data_ptr(), B, n_new, scale,
+                                         out.data_ptr(), _stream(stream))
+    _check(rc, "vt_prefill_attention")
+    return out
+
+
+def last_launches() -> int:
+    return int(attn_lib().vt_attn_last_launches())

@@ -1,0 +1,92 @@
+"""Decode attention + KV append on the B200 vs the CPU fp32 oracle (rows a27, a29).
+
+Tolerance: max|got - ref| / max|ref| <= 2e-2 (bf16 in, fp32 accumulate;
+BASELINE.json north_star). KV lives in real cuMemMap'd 2 MiB chunks under
+per-request VAs created by the manager; every request maps exactly
+ceil(len/tpc) chunks (no lookahead), so any read past the last mapped chunk
+would fault and fail the test.
+"""
+
+import zlib
+
+import pytest
+import torch
+
+from oracle.attention_ref import decode_attention_ref, rel_err
+from paper_2407_15309_b200.attention import DecodeWorkspace, decode_attention, kv_append, last_launches
+from vt_gpu_util import admit_with_lengths, cuda_stack, gather
+
+TOL = 2e-2
+
+CASES = {
+    # name: (layers, kv_heads, q_heads, max_seq, lens)
+    "toy_mha_cfg1": (1, 8, 8, 4096, [1, 63, 64, 65, 511, 512, 513, 700, 4095, 4096]),
+    "llama8b_gqa4": (32, 8, 32, 4352, [0, 1, 15, 16, 17, 100, 1000, 4096]),
+    "llama70b_shard_gqa8": (16, 2, 16, 4096, [5, 128, 129, 2049, 4096]),
+    "gqa2": (4, 4, 8, 2048, [33, 1024, 2000]),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("split", [0, 64, 4096])
+def test_decode_matches_oracle(cuda_ok, name, split):
+    layers, hkv, hq, max_seq, lens = CASES[name]
+    st = cuda_stack(layers, hkv, hq, max_seq)
+    kv_va, seq = admit_with_lengths(st, lens, seed=zlib.crc32(name.encode()) % 1000)
+    layer = layers - 1
+    q = torch.randn(len(lens), hq, 128, device="cuda").to(torch.bfloat16)
+    out = decode_attention(q, kv_va, seq, layer, st.geo, max(lens), split_tokens=split)
+    torch.cuda.synchronize()
+    assert last_launches() >= 1
+    ks, vs = gather(st, kv_va, lens, layer)
+    ref = decode_attention_ref(q.cpu(), ks, vs)
+    err = rel_err(out.cpu(), ref)
+    assert err <= TOL, f"{name} split={split}: rel err {err:.3e}"
+    for b, n in enumerate(lens):  # empty request -> zeros, never NaN
+        if n == 0:
+            assert torch.all(out[b] == 0)
+    assert torch.isfinite(out.float()).all()
+
+
+@pytest.mark.gpu
+def test_kv_append_then_decode(cuda_ok):
+    """Grow every request by one token through the manager (extend maps a new
+    chunk where needed), append its K/V with the kernel, decode over len+1."""
+    layers, hkv, hq = 32, 8, 32
+    lens = [15, 16, 31, 200]
+    st = cuda_stack(layers, hkv, hq, 4096)
+    kv_va, seq = admit_with_lengths(st, lens, seed=3)
+    for i, n in enumerate(lens):
+        st.sched.extend(f"req{i}", n + 1)
+    st.dev.wait()
+    k_new = torch.randn(layers, len(lens), hkv, 128, device="cuda").to(torch.bfloat16)
+    v_new = torch.randn_like(k_new)
+    pos = seq.clone()
+    kv_append(k_new, v_new, kv_va, pos, st.geo)
+    for i in range(len(lens)):
+        st.sched.append_token(f"req{i}", 1)
+    new_lens = [n + 1 for n in lens]
+    seq1 = torch.tensor(new_lens, dtype=torch.int32, device="cuda")
+    for layer in (0, 17, 31):
+        ks, vs = gather(st, kv_va, new_lens, layer)
+        for b, n in enumerate(lens):
+            assert torch.equal(ks[b][:, n], k_new[layer, b].cpu())
+            assert torch.equal(vs[b][:, n], v_new[layer, b].cpu())
+        q = torch.randn(len(lens), hq, 128, device="cuda").to(torch.bfloat16)
+        out = decode_attention(q, kv_va, seq1, layer, st.geo, max(new_lens))
+        ref = decode_attention_ref(q.cpu(), ks, vs)
+        assert rel_err(out.cpu(), ref) <= TOL
+
+
+@pytest.mark.gpu
+def test_decode_reuses_workspace_and_is_deterministic(cuda_ok):
+    st = cuda_stack(32, 8, 32, 4352)
+    lens = [4096] * 8
+    kv_va, seq = admit_with_lengths(st, lens, seed=9)
+    ws = DecodeWorkspace(st.geo, len(lens), 4096)
+    q = torch.randn(len(lens), 32, 128, device="cuda").to(torch.bfloat16)
+    a = decode_attention(q, kv_va, seq, 3, st.geo, 4096, workspace=ws)
+    b = decode_attention(q, kv_va, seq, 3, st.geo, 4096, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
