@@ -73,33 +73,43 @@ def parse():
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled in-process (NVML) every 50 ms
+    during the timed region; nvidia-smi subprocesses are too slow/intrusive."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40,
+    }
 
     def __init__(self, index: int) -> None:
         self.index = index
-        self.samples: list[list[str]] = []
+        self.samples: list[tuple[int, int, int]] = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
 
     def _run(self) -> None:
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:  # older bindings
+                    reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((sm, mx, reasons))
+                self._stop.wait(0.05)
+        except Exception as exc:  # pragma: no cover - no NVML
+            self._nvml = repr(exc)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.06)
         return self
 
     def __exit__(self, *exc):
@@ -109,14 +119,12 @@ class ClockSampler:
 
     def summary(self) -> dict:
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for s in self.samples for n, v in zip(names, s[4:8])
-                          if v.strip().lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": [f"nvml unavailable: {self._nvml}"]}
+        reasons = sorted({name for _, _, r in self.samples for name, bit in self.REASONS.items()
+                          if r & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
                 "reasons": reasons, "samples": len(self.samples)}
 
 
@@ -218,6 +226,8 @@ class DecodeWorkload:
         self.stream = torch.cuda.current_stream()
         self.host_lens = list(self.lens)
         self.stalls = 0
+        self.host_waits = 0
+        self.last_done = None
         self.extend_ns: list[int] = []
         self.chunks_mapped = 0
         self._issue_extends()  # capacity for the first step's token
@@ -246,6 +256,8 @@ class DecodeWorkload:
 
     # -- one step -------------------------------------------------------------
     def step(self, q=None, k_new=None, v_new=None, out=None, layer_events=None):
+        import torch
+
         from paper_2407_15309_b200.attention import decode_attention, kv_append
 
         q = self.q if q is None else q
@@ -254,7 +266,9 @@ class DecodeWorkload:
         out = self.out if out is None else out
         ticket = self.dev.ticket()
         if not self.dev.ready(ticket):
-            self.stalls += 1  # mapping not done when the launch was due
+            self.host_waits += 1
+            if self.last_done is not None and self.last_done.query():
+                self.stalls += 1  # GPU drained while this step's pages were still mapping
         self.dev.wait(ticket)
         kv_append(k_new, v_new, self.kv_va, self.seq, self.geo)
         self.seq.add_(1)
@@ -269,6 +283,8 @@ class DecodeWorkload:
                 layer_events[layer][1].record(self.stream)
             launches += 2 if math.ceil(mx / (self.split or 512)) > 1 else 1
         self.dev.fence(self.stream.cuda_stream)
+        self.last_done = torch.cuda.Event()
+        self.last_done.record(self.stream)
         for rid in self.rids:
             self.sched.append_token(rid, 1)
         self.host_lens = [n + 1 for n in self.host_lens]
@@ -298,6 +314,7 @@ def run_ours(args, world, rank, local):
     decode_bytes = 0
     launches = 0
     stalls0 = wl.stalls
+    waits0 = wl.host_waits
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
@@ -416,7 +433,9 @@ def run_ours(args, world, rank, local):
                 "host_submit_us_p99": round(ext[min(len(ext) - 1, int(len(ext) * 0.99))] / 1e3, 2),
                 "driver_map_us_mean": round(drv["map_ns_total"] / max(drv["map_calls"], 1) / 1e3, 2),
                 "driver_create_us_mean": round(drv["create_ns_total"] / max(drv["create_calls"], 1) / 1e3, 2),
-                "stalled_steps": stalls,
+                "driver_access_us_mean": round(drv["access_ns_total"] / max(drv["access_calls"], 1) / 1e3, 2),
+                "gpu_stalled_steps": stalls,
+                "host_waited_steps": wl.host_waits - waits0,
                 "hidden": stalls == 0,
             },
             "gpu_launches": launches + 0,

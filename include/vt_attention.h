@@ -58,14 +58,22 @@ int vt_kv_append(const vt_kv_geometry* g, int32_t layer_begin, int32_t n_layers,
                  const void* k_new, const void* v_new, const uint64_t* kv_va,
                  const int32_t* positions, int32_t batch, void* stream);
 
-/* Prefill / prefix-prefill (row a28): n_new query tokens per request at
- * positions [start_b, start_b + n_new) attend causally to KV [0, start_b + i]
- * already in the cache (prefix chunks shared through the rTree are mapped into
- * the request's own VA, so they are read in place).
- *   q   : [batch, n_new, q_heads, head_dim] bf16;  out : same shape
- *   start: [batch] i32 (shared prefix length, multiple of 128 for the tcgen05 path) */
+/* TMA descriptors for prefill (HOST function): one 128-byte CUtensorMap per
+ * request, written to maps_host (batch*128 bytes, 64-byte aligned), viewing
+ * va_host[b] as (d, token-in-chunk, (layer,K|V,head) block, chunk) with chunk
+ * extent ceil(kv_len_host[b] / tpc) — the TMA never reads unmapped VA. The
+ * caller copies the maps to device memory for vt_prefill_attention. */
+int vt_prefill_kv_maps(const vt_kv_geometry* g, const uint64_t* va_host,
+                       const int32_t* kv_len_host, int32_t batch, void* maps_host);
+
+/* Prefill / prefix-prefill (row a28), tcgen05/TMEM/TMA: n_new query tokens per
+ * request at positions [start_b, start_b + n_new) attend causally to KV
+ * [0, start_b + i] already in the cache (prefix chunks shared through the
+ * rTree are mapped into the request's own VA, so they are read in place).
+ *   q, out : [batch, n_new, q_heads, head_dim] bf16
+ *   kv_maps: device copy of vt_prefill_kv_maps output;  start : [batch] i32 */
 int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
-                         const uint64_t* kv_va, const int32_t* start, int32_t batch,
+                         const void* kv_maps, const int32_t* start, int32_t batch,
                          int32_t n_new, float scale, void* out, void* stream);
 
 /* Number of kernel launches the last call on this thread issued (bench

@@ -88,6 +88,7 @@ typedef struct vt_driver_stats {
   int64_t ops_completed;
   int64_t map_calls, unmap_calls, create_calls, destroy_calls, access_calls;
   int64_t map_ns_total, unmap_ns_total, create_ns_total, destroy_ns_total;
+  int64_t access_ns_total; /* cuMemSetAccess share of map_ns_total */
   int64_t fence_waits, fence_wait_ns_total;
   int64_t max_op_ns;
 } vt_driver_stats;

@@ -84,6 +84,7 @@ class VtDriverStats(ctypes.Structure):
         ("unmap_ns_total", c_int64),
         ("create_ns_total", c_int64),
         ("destroy_ns_total", c_int64),
+        ("access_ns_total", c_int64),
         ("fence_waits", c_int64),
         ("fence_wait_ns_total", c_int64),
         ("max_op_ns", c_int64),

@@ -47,6 +47,8 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_prefill_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, c_int32,
                                              c_float, P, P]
         lib.vt_prefill_attention.restype = c_int
+        lib.vt_prefill_kv_maps.argtypes = [POINTER(_Geo), P, P, c_int32, P]
+        lib.vt_prefill_kv_maps.restype = c_int
         lib.vt_attn_last_launches.argtypes = []
         lib.vt_attn_last_launches.restype = c_int32
         _lib = lib
@@ -54,7 +56,7 @@ def attn_lib() -> ctypes.CDLL:
 
 
 ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_workspace_bytes", "vt_kv_append",
-                "vt_prefill_attention", "vt_attn_last_launches")
+                "vt_prefill_kv_maps", "vt_prefill_attention", "vt_attn_last_launches")
 
 
 def _geo(g: KVGeometry) -> _Geo:
@@ -128,19 +130,38 @@ def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, kv_va: torch.Tensor,
     _check(rc, "vt_kv_append")
 
 
-def prefill_attention(q: torch.Tensor, kv_va: torch.Tensor, start: torch.Tensor, layer: int,
+def prefill_kv_maps(va: list[int], kv_len: list[int], geo: KVGeometry,
+                    device: str = "cuda") -> torch.Tensor:
+    """Per-request TMA descriptors over the request VAs (host encode, one H2D
+    copy). Chunk extent = ceil(kv_len/tpc): exactly the mapped, valid chunks."""
+    B = len(va)
+    raw = ctypes.create_string_buffer(B * 128 + 64)
+    addr = (ctypes.addressof(raw) + 63) & ~63
+    vas = (c_uint64 * B)(*va)
+    lens = (c_int32 * B)(*kv_len)
+    rc = attn_lib().vt_prefill_kv_maps(ctypes.byref(_geo(geo)), ctypes.addressof(vas),
+                                       ctypes.addressof(lens), B, addr)
+    _check(rc, "vt_prefill_kv_maps")
+    host = torch.frombuffer(bytearray(ctypes.string_at(addr, B * 128)), dtype=torch.uint8)
+    return host.to(device)
+
+
+def prefill_attention(q: torch.Tensor, kv_maps: torch.Tensor, start: torch.Tensor, layer: int,
                       geo: KVGeometry, out: torch.Tensor | None = None, scale: float | None = None,
                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """q ``[B, n_new, Hq, d]``: new tokens at ``[start_b, start_b + n_new)``
-    attend causally to the KV already in the cache (shared prefix included)."""
+    attend causally to the KV already in the cache (shared prefix included);
+    ``kv_maps`` from :func:`prefill_kv_maps` with kv_len = start + n_new."""
     B, n_new = q.shape[0], q.shape[1]
+    if q.dtype != torch.bfloat16 or q.shape[2:] != (geo.q_heads, geo.head_dim):
+        raise ValueError(f"q must be bf16 [B, n_new, {geo.q_heads}, {geo.head_dim}]")
     if out is None:
         out = torch.empty_like(q)
-    _need_cuda(q, kv_va, start, out)
+    _need_cuda(q, kv_maps, start, out)
     if scale is None:
         scale = 1.0 / math.sqrt(geo.head_dim)
     rc = attn_lib().vt_prefill_attention(ctypes.byref(_geo(geo)), layer, q.data_ptr(),
-                                         kv_va.data_ptr(), start.data_ptr(), B, n_new, scale,
+                                         kv_maps.data_ptr(), start.data_ptr(), B, n_new, scale,
                                          out.data_ptr(), _stream(stream))
     _check(rc, "vt_prefill_attention")
     return out

@@ -231,21 +231,32 @@ struct vt_device {
     return true;
   }
 
-  void submit(DrvOp op) {
+  // Ops are queued in issue order; kick() hands everything queued so far to
+  // the worker (async) or executes it inline as one batch (sync), so a batched
+  // map of consecutive pages always costs a single cuMemSetAccess.
+  void enqueue(DrvOp op) {
     op.submit_ns = now_ns();
     op.fence_epoch = fence_epoch;
-    if (!async) {
-      op.ticket = ++next_ticket;
-      execute_run(&op, 1);
-      done_ticket.store(op.ticket);
+    std::lock_guard<std::mutex> lk(mu);
+    op.ticket = ++next_ticket;
+    queue.push_back(op);
+  }
+
+  void kick() {
+    if (!is_cuda()) return;
+    if (async) {
+      cv_work.notify_one();
       return;
     }
+    std::vector<DrvOp> batch;
     {
       std::lock_guard<std::mutex> lk(mu);
-      op.ticket = ++next_ticket;
-      queue.push_back(op);
+      batch.assign(queue.begin(), queue.end());
+      queue.clear();
     }
-    cv_work.notify_one();
+    if (batch.empty()) return;
+    execute_run(batch.data(), batch.size());
+    done_ticket.store(batch.back().ticket);
   }
 
   void record_error(const std::string& what) {
@@ -306,9 +317,11 @@ struct vt_device {
             run_len += static_cast<size_t>(cfg.chunk_bytes);
             ++j;
           }
+          int64_t ta = now_ns();
           CUresult r = d.MemSetAccess(run_start, run_len, &access, 1);
           if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
           dstats.access_calls++;
+          dstats.access_ns_total += now_ns() - ta;
           dstats.map_ns_total += now_ns() - t0;
           i = j;
           break;
@@ -401,7 +414,7 @@ int do_map(vt_device* d, int64_t base, int64_t page, int64_t id) {
     op.kind = DrvKind::kMap;
     op.handle_id = id;
     op.addr = rs->va + static_cast<CUdeviceptr>(page) * static_cast<CUdeviceptr>(d->cfg.chunk_bytes);
-    d->submit(op);
+    d->enqueue(op);
   }
   return VT_OK;
 }
@@ -424,7 +437,7 @@ int do_unmap(vt_device* d, int64_t base, int64_t page, int64_t* id_out) {
     DrvOp op{};
     op.kind = DrvKind::kUnmap;
     op.addr = rs.va + static_cast<CUdeviceptr>(page) * static_cast<CUdeviceptr>(d->cfg.chunk_bytes);
-    d->submit(op);
+    d->enqueue(op);
   }
   if (id_out) *id_out = id;
   return VT_OK;
@@ -563,7 +576,8 @@ int vt_create_chunk(vt_device* d, int64_t* id) {
     DrvOp op{};
     op.kind = DrvKind::kCreate;
     op.handle_id = h;
-    d->submit(op);
+    d->enqueue(op);
+    d->kick();
   }
   *id = h;
   return VT_OK;
@@ -571,7 +585,9 @@ int vt_create_chunk(vt_device* d, int64_t* id) {
 
 // device.py:218-233
 int vt_map_page(vt_device* d, int64_t base, int64_t page, int64_t id) {
-  return do_map(d, base, page, id);
+  int rc = do_map(d, base, page, id);
+  d->kick();
+  return rc;
 }
 
 int vt_map_pages(vt_device* d, int64_t base, int64_t first_page, const int64_t* ids, int64_t n,
@@ -583,12 +599,15 @@ int vt_map_pages(vt_device* d, int64_t base, int64_t first_page, const int64_t* 
     if (rc) break;
   }
   if (n_done) *n_done = k;
+  d->kick();
   return rc;
 }
 
 // device.py:235-245
 int vt_unmap_page(vt_device* d, int64_t base, int64_t page, int64_t* id) {
-  return do_unmap(d, base, page, id);
+  int rc = do_unmap(d, base, page, id);
+  d->kick();
+  return rc;
 }
 
 int vt_unmap_tail(vt_device* d, int64_t base, int64_t from_page, int64_t down_to, int64_t* ids,
@@ -600,6 +619,7 @@ int vt_unmap_tail(vt_device* d, int64_t base, int64_t from_page, int64_t down_to
     if (rc) break;
   }
   if (n_done) *n_done = k;
+  d->kick();
   return rc;
 }
 
@@ -616,7 +636,8 @@ int vt_release(vt_device* d, int64_t base) {
     op.kind = DrvKind::kRelease;
     op.addr = it->second.va;
     op.size = static_cast<size_t>(it->second.pages * d->cfg.chunk_bytes);
-    d->submit(op);
+    d->enqueue(op);
+    d->kick();
   }
   d->reserved_bytes -= it->second.pages * d->cfg.chunk_bytes;
   d->ranges.erase(it);
@@ -639,7 +660,8 @@ int vt_destroy_chunk(vt_device* d, int64_t id) {
     DrvOp op{};
     op.kind = DrvKind::kDestroy;
     op.handle_id = id;
-    d->submit(op);
+    d->enqueue(op);
+    d->kick();
   }
   return VT_OK;
 }
