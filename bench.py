@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=list(CONFIGS), default="llama3-8b-decode")
     ap.add_argument("--split", type=int, default=0, help="split-KV tokens per CTA (0=auto)")
+    ap.add_argument("--path", choices=["tcgen05", "cuda_core"], default="tcgen05",
+                    help="decode kernel: tcgen05/TMEM (default) or CUDA-core FFMA2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
@@ -178,11 +180,11 @@ def sum_over_ranks(x: float, world: int) -> float:
 class DecodeWorkload:
     """64 requests of one GPU, their vTensor spaces, and the per-step driver."""
 
-    def __init__(self, cfg_name: str, split: int, seed: int):
+    def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05"):
         import torch
 
         import paper_2407_15309_b200 as vt
-        from paper_2407_15309_b200.attention import DecodeWorkspace
+        from paper_2407_15309_b200.attention import DecodeWorkspace, KVMapCache
         from paper_2407_15309_b200.kv_layout import KVGeometry, chunk_view
 
         L, hkv, hq, B, ctx = CONFIGS[cfg_name]
@@ -222,7 +224,10 @@ class DecodeWorkload:
         self.v_new = torch.randn_like(self.k_new)
         self.out = torch.empty_like(self.q)
         self.split = split
+        self.path = path
         self.ws = DecodeWorkspace(self.geo, B, self.max_seq, split)
+        self.vas = vas
+        self.maps = KVMapCache(self.geo, B) if path == "tcgen05" else None
         self.stream = torch.cuda.current_stream()
         self.host_lens = list(self.lens)
         self.stalls = 0
@@ -258,7 +263,7 @@ class DecodeWorkload:
     def step(self, q=None, k_new=None, v_new=None, out=None, layer_events=None):
         import torch
 
-        from paper_2407_15309_b200.attention import decode_attention, kv_append
+        from paper_2407_15309_b200.attention import decode_attention, kv_append, last_launches
 
         q = self.q if q is None else q
         k_new = self.k_new if k_new is None else k_new
@@ -270,6 +275,11 @@ class DecodeWorkload:
             if self.last_done is not None and self.last_done.query():
                 self.stalls += 1  # GPU drained while this step's pages were still mapping
         self.dev.wait(ticket)
+        kv_maps = None
+        if self.maps is not None:  # TMA descriptors follow the newly mapped chunks
+            tpc = self.cfg.tokens_per_chunk
+            kv_maps = self.maps.update(
+                self.vas, [self.sched.mem[r].vt.space.mapped_pages * tpc for r in self.rids])
         kv_append(k_new, v_new, self.kv_va, self.seq, self.geo)
         self.seq.add_(1)
         mx = max(self.host_lens) + 1
@@ -278,10 +288,11 @@ class DecodeWorkload:
             if layer_events is not None:
                 layer_events[layer][0].record(self.stream)
             decode_attention(q[layer], self.kv_va, self.seq, layer, self.geo, mx,
-                             out=out[layer], workspace=self.ws, split_tokens=self.split)
+                             out=out[layer], workspace=self.ws, split_tokens=self.split,
+                             kv_maps=kv_maps)
             if layer_events is not None:
                 layer_events[layer][1].record(self.stream)
-            launches += 2 if math.ceil(mx / (self.split or 512)) > 1 else 1
+            launches += last_launches()
         self.dev.fence(self.stream.cuda_stream)
         self.last_done = torch.cuda.Event()
         self.last_done.record(self.stream)
@@ -295,7 +306,7 @@ class DecodeWorkload:
 def run_ours(args, world, rank, local):
     import torch
 
-    wl = DecodeWorkload(args.config, args.split, seed=1234 + rank)
+    wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path)
     if args.profile_steps:
         for _ in range(args.profile_steps):
             wl.step()
@@ -315,6 +326,9 @@ def run_ours(args, world, rank, local):
     launches = 0
     stalls0 = wl.stalls
     waits0 = wl.host_waits
+    drv0 = wl.dev.driver_stats()
+    wl.extend_ns.clear()
+    mapped0 = wl.chunks_mapped
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
@@ -368,7 +382,8 @@ def run_ours(args, world, rank, local):
                "h2d_bytes_per_step": int((host_q.numel() + host_k.numel() + host_v.numel()) * 2),
                "d2h_bytes_per_step": int(host_o.numel() * 2)}
 
-    drv = wl.dev.driver_stats()
+    drv_end = wl.dev.driver_stats()
+    drv = {k: drv_end[k] - drv0[k] for k in drv_end}  # timed region only
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
@@ -411,13 +426,15 @@ def run_ours(args, world, rank, local):
                 "parallelism": f"request-partition x{world} (no collective)",
                 "l2": "inputs larger than L2 (KV working set %.1f GiB)" % (
                     sum(wl.host_lens) * wl.cfg.bytes_per_token / GIB),
-                "split_tokens": args.split or 512,
+                "split_tokens": args.split or "auto",
+                "decode_path": args.path,
             },
             "tokens_per_s": round(tokens_all / (elapsed_max * 1e-3), 1),
             "hbm_frac_of_step": round(value / hbm_peak, 4),
             "roofline": {
                 "bound": "hbm",
-                "kernel": "vt::decode_splitkv_kernel<4>",
+                "kernel": ("vt::dtc::decode_tc_kernel" if args.path == "tcgen05"
+                           else "vt::decode_splitkv_kernel<4>"),
                 "achieved": round(achieved, 1),
                 "peak": hbm_peak,
                 "peak_source": peak_src,
@@ -428,7 +445,7 @@ def run_ours(args, world, rank, local):
                 "algorithmic_bytes_per_launch": int(decode_bytes / n_decode),
             },
             "extend": {
-                "chunks_mapped": wl.chunks_mapped,
+                "chunks_mapped": wl.chunks_mapped - mapped0,
                 "host_submit_us_p50": round(ext[len(ext) // 2] / 1e3, 2),
                 "host_submit_us_p99": round(ext[min(len(ext) - 1, int(len(ext) * 0.99))] / 1e3, 2),
                 "driver_map_us_mean": round(drv["map_ns_total"] / max(drv["map_calls"], 1) / 1e3, 2),

@@ -41,13 +41,16 @@ typedef struct vt_kv_geometry {
  * out[b,h,:] = softmax(scale * q[b,h,:] . K[b, 0:len_b, h/G]^T) V[b, 0:len_b, h/G].
  *   q, out   : [batch, q_heads, head_dim] bf16
  *   kv_va    : [batch] u64 request VAs;  seq_lens : [batch] i32
+ *   kv_maps  : NULL -> CUDA-core path (cp.async.bulk ring, FFMA2);
+ *              else device copy of vt_kv_tensor_maps(...) -> tcgen05/TMEM path
  *   max_seq_len: host upper bound of seq_lens (sizes the split grid)
  *   workspace: >= vt_decode_workspace_bytes(...) bytes (fp32 split partials)
- *   split_tokens: KV tokens per CTA work unit (multiple of 64), 0 = default */
+ *   split_tokens: KV tokens per work unit (multiple of 128), 0 = default */
 int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
-                        const uint64_t* kv_va, const int32_t* seq_lens, int32_t batch,
-                        int32_t max_seq_len, float scale, void* out, void* workspace,
-                        size_t workspace_bytes, int32_t split_tokens, void* stream);
+                        const uint64_t* kv_va, const void* kv_maps, const int32_t* seq_lens,
+                        int32_t batch, int32_t max_seq_len, float scale, void* out,
+                        void* workspace, size_t workspace_bytes, int32_t split_tokens,
+                        void* stream);
 size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t batch, int32_t max_seq_len,
                                  int32_t split_tokens);
 
@@ -58,20 +61,22 @@ int vt_kv_append(const vt_kv_geometry* g, int32_t layer_begin, int32_t n_layers,
                  const void* k_new, const void* v_new, const uint64_t* kv_va,
                  const int32_t* positions, int32_t batch, void* stream);
 
-/* TMA descriptors for prefill (HOST function): one 128-byte CUtensorMap per
- * request, written to maps_host (batch*128 bytes, 64-byte aligned), viewing
- * va_host[b] as (d, token-in-chunk, (layer,K|V,head) block, chunk) with chunk
- * extent ceil(kv_len_host[b] / tpc) — the TMA never reads unmapped VA. The
- * caller copies the maps to device memory for vt_prefill_attention. */
-int vt_prefill_kv_maps(const vt_kv_geometry* g, const uint64_t* va_host,
-                       const int32_t* kv_len_host, int32_t batch, void* maps_host);
+/* TMA descriptors over the request VAs (HOST function): one 128-byte
+ * CUtensorMap per request, written to maps_host (batch*128 bytes, 64-byte
+ * aligned), viewing va_host[b] as (d, token-in-chunk, (layer,K|V,head) block,
+ * chunk) with chunk extent ceil(n_tokens_host[b] / tpc) — pass the mapped
+ * token capacity (mapped_pages*tpc) or the valid length: the TMA never reads
+ * unmapped VA. The caller copies the maps to device memory. A map only
+ * changes when its request maps a new chunk (the VA itself never moves). */
+int vt_kv_tensor_maps(const vt_kv_geometry* g, const uint64_t* va_host,
+                      const int32_t* n_tokens_host, int32_t batch, void* maps_host);
 
 /* Prefill / prefix-prefill (row a28), tcgen05/TMEM/TMA: n_new query tokens per
  * request at positions [start_b, start_b + n_new) attend causally to KV
  * [0, start_b + i] already in the cache (prefix chunks shared through the
  * rTree are mapped into the request's own VA, so they are read in place).
  *   q, out : [batch, n_new, q_heads, head_dim] bf16
- *   kv_maps: device copy of vt_prefill_kv_maps output;  start : [batch] i32 */
+ *   kv_maps: device copy of vt_kv_tensor_maps output;  start : [batch] i32 */
 int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                          const void* kv_maps, const int32_t* start, int32_t batch,
                          int32_t n_new, float scale, void* out, void* stream);

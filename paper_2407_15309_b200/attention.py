@@ -37,7 +37,7 @@ def attn_lib() -> ctypes.CDLL:
     if _lib is None:
         lib = _load("libvtattn.so")
         P = c_void_p
-        lib.vt_decode_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, c_int32,
+        lib.vt_decode_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, P, c_int32, c_int32,
                                             c_float, P, P, c_size_t, c_int32, P]
         lib.vt_decode_attention.restype = c_int
         lib.vt_decode_workspace_bytes.argtypes = [POINTER(_Geo), c_int32, c_int32, c_int32]
@@ -47,8 +47,8 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_prefill_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, c_int32,
                                              c_float, P, P]
         lib.vt_prefill_attention.restype = c_int
-        lib.vt_prefill_kv_maps.argtypes = [POINTER(_Geo), P, P, c_int32, P]
-        lib.vt_prefill_kv_maps.restype = c_int
+        lib.vt_kv_tensor_maps.argtypes = [POINTER(_Geo), P, P, c_int32, P]
+        lib.vt_kv_tensor_maps.restype = c_int
         lib.vt_attn_last_launches.argtypes = []
         lib.vt_attn_last_launches.restype = c_int32
         _lib = lib
@@ -56,7 +56,7 @@ def attn_lib() -> ctypes.CDLL:
 
 
 ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_workspace_bytes", "vt_kv_append",
-                "vt_prefill_kv_maps", "vt_prefill_attention", "vt_attn_last_launches")
+                "vt_kv_tensor_maps", "vt_prefill_attention", "vt_attn_last_launches")
 
 
 def _geo(g: KVGeometry) -> _Geo:
@@ -88,18 +88,22 @@ class DecodeWorkspace:
         self.geo, self.split_tokens = geo, split_tokens
         nbytes = attn_lib().vt_decode_workspace_bytes(ctypes.byref(_geo(geo)), batch,
                                                        max_seq_len, split_tokens)
-        self.buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        # zeroed: the tail holds the self-resetting split-arrival counters
+        self.buf = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=device)
         self.batch, self.max_seq_len = batch, max_seq_len
 
 
 def decode_attention(q: torch.Tensor, kv_va: torch.Tensor, seq_lens: torch.Tensor, layer: int,
                      geo: KVGeometry, max_seq_len: int, out: torch.Tensor | None = None,
                      workspace: DecodeWorkspace | None = None, scale: float | None = None,
-                     split_tokens: int = 0, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                     split_tokens: int = 0, stream: torch.cuda.Stream | None = None,
+                     kv_maps: torch.Tensor | None = None) -> torch.Tensor:
     """q ``[B, Hq, d]`` bf16 -> out ``[B, Hq, d]`` bf16 for one layer.
 
     ``kv_va`` is an int64 CUDA tensor of request VAs (``device.va(space.rng)``),
-    ``seq_lens`` an int32 CUDA tensor; ``max_seq_len`` a host bound on it."""
+    ``seq_lens`` an int32 CUDA tensor; ``max_seq_len`` a host bound on it.
+    With ``kv_maps`` (:class:`KVMapCache`) the tcgen05/TMEM kernel runs;
+    without, the CUDA-core cp.async.bulk kernel."""
     B = q.shape[0]
     if q.dtype != torch.bfloat16 or q.shape[1:] != (geo.q_heads, geo.head_dim):
         raise ValueError(f"q must be bf16 [B, {geo.q_heads}, {geo.head_dim}]")
@@ -110,8 +114,13 @@ def decode_attention(q: torch.Tensor, kv_va: torch.Tensor, seq_lens: torch.Tenso
     _need_cuda(q, kv_va, seq_lens, out)
     if scale is None:
         scale = 1.0 / math.sqrt(geo.head_dim)
+    maps_ptr = None
+    if kv_maps is not None:
+        _need_cuda(kv_maps)
+        maps_ptr = kv_maps.data_ptr()
     rc = attn_lib().vt_decode_attention(
-        ctypes.byref(_geo(geo)), layer, q.data_ptr(), kv_va.data_ptr(), seq_lens.data_ptr(), B,
+        ctypes.byref(_geo(geo)), layer, q.data_ptr(), kv_va.data_ptr(), maps_ptr,
+        seq_lens.data_ptr(), B,
         max_seq_len, scale, out.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(),
         workspace.split_tokens or split_tokens, _stream(stream))
     _check(rc, "vt_decode_attention")
@@ -130,20 +139,74 @@ def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, kv_va: torch.Tensor,
     _check(rc, "vt_kv_append")
 
 
-def prefill_kv_maps(va: list[int], kv_len: list[int], geo: KVGeometry,
-                    device: str = "cuda") -> torch.Tensor:
+def kv_tensor_maps(va: list[int], n_tokens: list[int], geo: KVGeometry,
+                   device: str = "cuda") -> torch.Tensor:
     """Per-request TMA descriptors over the request VAs (host encode, one H2D
-    copy). Chunk extent = ceil(kv_len/tpc): exactly the mapped, valid chunks."""
+    copy). Chunk extent = ceil(n_tokens/tpc) — pass valid or mapped tokens."""
     B = len(va)
     raw = ctypes.create_string_buffer(B * 128 + 64)
     addr = (ctypes.addressof(raw) + 63) & ~63
     vas = (c_uint64 * B)(*va)
-    lens = (c_int32 * B)(*kv_len)
-    rc = attn_lib().vt_prefill_kv_maps(ctypes.byref(_geo(geo)), ctypes.addressof(vas),
-                                       ctypes.addressof(lens), B, addr)
-    _check(rc, "vt_prefill_kv_maps")
+    lens = (c_int32 * B)(*n_tokens)
+    rc = attn_lib().vt_kv_tensor_maps(ctypes.byref(_geo(geo)), ctypes.addressof(vas),
+                                      ctypes.addressof(lens), B, addr)
+    _check(rc, "vt_kv_tensor_maps")
     host = torch.frombuffer(bytearray(ctypes.string_at(addr, B * 128)), dtype=torch.uint8)
     return host.to(device)
+
+
+prefill_kv_maps = kv_tensor_maps
+
+
+class KVMapCache:
+    """Device array of per-request TMA descriptors, re-encoded only for the
+    requests whose mapped-chunk count changed (the VA never moves, so a
+    request's descriptor changes once per newly mapped 2 MiB chunk).
+
+    Uploads go through a ring of pinned staging buffers guarded by CUDA
+    events, so an update never blocks the host on in-flight GPU work."""
+
+    RING = 4
+
+    def __init__(self, geo: KVGeometry, batch: int, device: str = "cuda") -> None:
+        self.geo, self.batch = geo, batch
+        self._raw = ctypes.create_string_buffer(batch * 128 + 64)
+        self._addr = (ctypes.addressof(self._raw) + 63) & ~63
+        self._key: list[tuple[int, int] | None] = [None] * batch
+        self._host = [torch.empty(batch * 128, dtype=torch.uint8, pin_memory=True)
+                      for _ in range(self.RING)]
+        self._done: list[torch.cuda.Event | None] = [None] * self.RING
+        self._slot = 0
+        self.dev = torch.empty(batch * 128, dtype=torch.uint8, device=device)
+        self.encodes = 0
+
+    def update(self, va: list[int], mapped_tokens: list[int],
+               stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        changed = [i for i in range(self.batch) if self._key[i] != (va[i], mapped_tokens[i])]
+        if not changed:
+            return self.dev
+        g = ctypes.byref(_geo(self.geo))
+        for i in changed:
+            vas = (c_uint64 * 1)(va[i])
+            n = (c_int32 * 1)(mapped_tokens[i])
+            rc = attn_lib().vt_kv_tensor_maps(g, ctypes.addressof(vas), ctypes.addressof(n), 1,
+                                              self._addr + 128 * i)
+            _check(rc, "vt_kv_tensor_maps")
+            self._key[i] = (va[i], mapped_tokens[i])
+        self.encodes += len(changed)
+        slot = self._slot
+        self._slot = (slot + 1) % self.RING
+        if self._done[slot] is not None:
+            self._done[slot].synchronize()  # copy issued RING updates ago
+        host = self._host[slot]
+        ctypes.memmove(host.data_ptr(), self._addr, self.batch * 128)
+        st = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            self.dev.copy_(host, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        self._done[slot] = ev
+        return self.dev
 
 
 def prefill_attention(q: torch.Tensor, kv_maps: torch.Tensor, start: torch.Tensor, layer: int,

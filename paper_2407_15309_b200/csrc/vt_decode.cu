@@ -382,28 +382,54 @@ static thread_local int32_t g_last_launches = 0;
 
 extern "C" int32_t vt_attn_last_launches(void) { return g_last_launches; }
 
-static int default_split(int32_t max_seq_len) {
-  (void)max_seq_len;
-  return 512;
+static int default_split(int32_t max_seq_len, bool tcgen05) {
+  // tcgen05 (persistent): long units amortise the per-unit prologue; >= 2
+  // splits per (request, kv head) keep ~7 units per SM at batch 64.
+  // CUDA-core (one CTA per unit): ~4 units per (request, kv head) at 4k.
+  if (tcgen05) return max_seq_len >= 8192 ? 4096 : max_seq_len >= 4096 ? 2048 : 512;
+  return max_seq_len >= 4096 ? 1024 : 512;
+}
+
+static size_t counters_bytes(int32_t batch, int32_t hkv) {
+  return (static_cast<size_t>(batch) * hkv * sizeof(int32_t) + 255) & ~static_cast<size_t>(255);
 }
 
 extern "C" size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t batch,
                                             int32_t max_seq_len, int32_t split_tokens) {
-  const int split = split_tokens > 0 ? split_tokens : default_split(max_seq_len);
+  // sized for the smaller default split so one workspace serves both paths
+  const int split = split_tokens > 0 ? split_tokens : default_split(max_seq_len, false);
   const int64_t n_splits = (max_seq_len + split - 1) / split;
   const int64_t units = static_cast<int64_t>(batch) * g->kv_heads * n_splits;
   const int64_t G = g->q_heads / g->kv_heads;
-  return static_cast<size_t>(units * G * (kD + 2) * sizeof(float));
+  // [arrival counters, one per (request, kv head), 256-B padded][partial o][m, l]
+  return counters_bytes(batch, g->kv_heads) + static_cast<size_t>(units * G * (kD + 2) * sizeof(float));
+}
+
+int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
+                        const void* kv_maps, const int32_t* seq_lens, int32_t batch,
+                        int32_t n_splits, int32_t split, float scale, void* out, float* part_o,
+                        float* part_ml, int32_t* arrivals, int32_t n_sms, cudaStream_t stream);
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
 }
 
 extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
-                                   const uint64_t* kv_va, const int32_t* seq_lens, int32_t batch,
-                                   int32_t max_seq_len, float scale, void* out, void* workspace,
-                                   size_t workspace_bytes, int32_t split_tokens, void* stream) {
+                                   const uint64_t* kv_va, const void* kv_maps,
+                                   const int32_t* seq_lens, int32_t batch, int32_t max_seq_len,
+                                   float scale, void* out, void* workspace, size_t workspace_bytes,
+                                   int32_t split_tokens, void* stream) {
   g_last_launches = 0;
   if (g->head_dim != kD || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
   const int G = g->q_heads / g->kv_heads;
-  const int split = split_tokens > 0 ? split_tokens : default_split(max_seq_len);
+  const int split =
+      split_tokens > 0 ? split_tokens : default_split(max_seq_len, kv_maps != nullptr);
   if (split % kStageTok) return cudaErrorInvalidValue;
   if (batch <= 0 || max_seq_len <= 0) return 0;
   const int n_splits = (max_seq_len + split - 1) / split;
@@ -415,7 +441,9 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
   a.seq_lens = seq_lens;
   a.out = static_cast<__nv_bfloat16*>(out);
   const int64_t units = static_cast<int64_t>(batch) * g->kv_heads * n_splits;
-  a.part_o = static_cast<float*>(workspace);
+  int32_t* arrivals = static_cast<int32_t*>(workspace);
+  a.part_o = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) +
+                                      counters_bytes(batch, g->kv_heads));
   a.part_ml = a.part_o + units * G * kD;
   a.batch = batch;
   a.hkv = g->kv_heads;
@@ -430,7 +458,12 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   dim3 grid(n_splits, g->kv_heads, batch);
   cudaError_t e;
-  switch (G) {
+  if (kv_maps != nullptr && batch <= 1024) {  // tcgen05 path (TMA maps over the request VAs)
+    int rc = vt_launch_decode_tc(g, layer, q, kv_maps, seq_lens, batch, n_splits, split, scale,
+                                 out, a.part_o, a.part_ml, arrivals, num_sms(), st);
+    g_last_launches = 1;
+    return rc;
+  } else switch (G) {
     case 1: e = launch_decode<1>(a, grid, st); break;
     case 2: e = launch_decode<2>(a, grid, st); break;
     case 4: e = launch_decode<4>(a, grid, st); break;

@@ -30,7 +30,7 @@
 #include <stdint.h>
 
 #include "../../include/vt_attention.h"
-#include "vt_common.cuh"
+#include "vt_tc_common.cuh"
 
 namespace vt {
 namespace pf {
@@ -388,62 +388,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ------------------------------------------------------------ host helpers --
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encoder() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(p);
-  }
-  return fn;
-}
-
-int encode(CUtensorMap* m, void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-           const cuuint32_t* box) {
-  EncodeFn fn = encoder();
-  if (!fn) return cudaErrorNotSupported;
-  cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : cudaErrorInvalidValue;
-}
-
 }  // namespace pf
 }  // namespace vt
 
 using namespace vt::pf;
-
-extern "C" int vt_prefill_kv_maps(const vt_kv_geometry* g, const uint64_t* va_host,
-                                  const int32_t* kv_len_host, int32_t batch, void* maps_host) {
-  if (g->head_dim != D) return cudaErrorInvalidValue;
-  const int tpc = g->tokens_per_chunk;
-  if (!((tpc < BN && BN % tpc == 0) || (tpc >= BN && tpc % BN == 0))) return cudaErrorInvalidValue;
-  auto* maps = static_cast<CUtensorMap*>(maps_host);
-  for (int b = 0; b < batch; ++b) {
-    const cuuint64_t n_chunks = static_cast<cuuint64_t>((kv_len_host[b] + tpc - 1) / tpc);
-    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(tpc),
-                                static_cast<cuuint64_t>(2 * g->layers * g->kv_heads),
-                                n_chunks > 0 ? n_chunks : 1};
-    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(D * 2),
-                                   static_cast<cuuint64_t>(tpc) * D * 2,
-                                   static_cast<cuuint64_t>(g->chunk_bytes)};
-    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(tpc < BN ? tpc : BN), 1,
-                               static_cast<cuuint32_t>(tpc < BN ? BN / tpc : 1)};
-    int rc = encode(&maps[b], reinterpret_cast<void*>(va_host[b]), 4, dims, strides, box);
-    if (rc) return rc;
-  }
-  return 0;
-}
 
 extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                                     const void* kv_maps, const int32_t* start, int32_t batch,
@@ -457,7 +405,7 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
                                  static_cast<cuuint64_t>(g->q_heads) * D * 2,
                                  static_cast<cuuint64_t>(n_new) * g->q_heads * D * 2};
   const cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(BM), 1};
-  int rc = encode(&qmap, const_cast<void*>(q), 4, dims, strides, box);
+  int rc = vt::encode_tensor_map_bf16(&qmap, const_cast<void*>(q), 4, dims, strides, box);
   if (rc) return rc;
   Args a{};
   a.out = static_cast<__nv_bfloat16*>(out);

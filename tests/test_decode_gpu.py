@@ -13,7 +13,8 @@ import pytest
 import torch
 
 from oracle.attention_ref import decode_attention_ref, rel_err
-from paper_2407_15309_b200.attention import DecodeWorkspace, decode_attention, kv_append, last_launches
+from paper_2407_15309_b200.attention import (DecodeWorkspace, decode_attention, kv_append,
+                                             kv_tensor_maps, last_launches)
 from vt_gpu_util import admit_with_lengths, cuda_stack, gather
 
 TOL = 2e-2
@@ -27,22 +28,32 @@ CASES = {
 }
 
 
+def mapped_maps(st, kv_va, n):
+    """TMA descriptors with chunk extent = the mapped prefix of each space."""
+    tpc = st.cfg.tokens_per_chunk
+    mapped = [st.sched.mem[f"req{i}"].vt.space.mapped_pages * tpc for i in range(n)]
+    return kv_tensor_maps(kv_va.tolist(), mapped, st.geo)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("split", [0, 64, 4096])
-def test_decode_matches_oracle(cuda_ok, name, split):
+@pytest.mark.parametrize("path,split", [("cuda_core", 0), ("cuda_core", 64), ("cuda_core", 4096),
+                                        ("tcgen05", 0), ("tcgen05", 128), ("tcgen05", 4096)])
+def test_decode_matches_oracle(cuda_ok, name, path, split):
     layers, hkv, hq, max_seq, lens = CASES[name]
     st = cuda_stack(layers, hkv, hq, max_seq)
     kv_va, seq = admit_with_lengths(st, lens, seed=zlib.crc32(name.encode()) % 1000)
     layer = layers - 1
     q = torch.randn(len(lens), hq, 128, device="cuda").to(torch.bfloat16)
-    out = decode_attention(q, kv_va, seq, layer, st.geo, max(lens), split_tokens=split)
+    maps = mapped_maps(st, kv_va, len(lens)) if path == "tcgen05" else None
+    out = decode_attention(q, kv_va, seq, layer, st.geo, max(lens), split_tokens=split,
+                           kv_maps=maps)
     torch.cuda.synchronize()
     assert last_launches() >= 1
     ks, vs = gather(st, kv_va, lens, layer)
     ref = decode_attention_ref(q.cpu(), ks, vs)
     err = rel_err(out.cpu(), ref)
-    assert err <= TOL, f"{name} split={split}: rel err {err:.3e}"
+    assert err <= TOL, f"{name} {path} split={split}: rel err {err:.3e}"
     for b, n in enumerate(lens):  # empty request -> zeros, never NaN
         if n == 0:
             assert torch.all(out[b] == 0)
@@ -74,8 +85,11 @@ def test_kv_append_then_decode(cuda_ok):
             assert torch.equal(ks[b][:, n], k_new[layer, b].cpu())
             assert torch.equal(vs[b][:, n], v_new[layer, b].cpu())
         q = torch.randn(len(lens), hq, 128, device="cuda").to(torch.bfloat16)
-        out = decode_attention(q, kv_va, seq1, layer, st.geo, max(new_lens))
         ref = decode_attention_ref(q.cpu(), ks, vs)
+        out = decode_attention(q, kv_va, seq1, layer, st.geo, max(new_lens))
+        assert rel_err(out.cpu(), ref) <= TOL
+        out = decode_attention(q, kv_va, seq1, layer, st.geo, max(new_lens),
+                               kv_maps=mapped_maps(st, kv_va, len(lens)))
         assert rel_err(out.cpu(), ref) <= TOL
 
 
@@ -88,5 +102,9 @@ def test_decode_reuses_workspace_and_is_deterministic(cuda_ok):
     q = torch.randn(len(lens), 32, 128, device="cuda").to(torch.bfloat16)
     a = decode_attention(q, kv_va, seq, 3, st.geo, 4096, workspace=ws)
     b = decode_attention(q, kv_va, seq, 3, st.geo, 4096, workspace=ws)
+    maps = mapped_maps(st, kv_va, len(lens))
+    c = decode_attention(q, kv_va, seq, 3, st.geo, 4096, workspace=ws, kv_maps=maps)
+    d = decode_attention(q, kv_va, seq, 3, st.geo, 4096, workspace=ws, kv_maps=maps)
     torch.cuda.synchronize()
-    assert torch.equal(a, b)
+    assert torch.equal(a, b) and torch.equal(c, d)
+    assert (a.float() - c.float()).abs().max() <= 2e-2 * a.float().abs().max()

@@ -11,7 +11,7 @@ import pytest
 import torch
 
 from oracle.attention_ref import prefill_attention_ref, rel_err
-from paper_2407_15309_b200.attention import prefill_attention, prefill_kv_maps
+from paper_2407_15309_b200.attention import kv_tensor_maps, prefill_attention
 from paper_2407_15309_b200.kv_layout import chunk_view, read_kv
 from vt_gpu_util import cuda_stack
 
@@ -83,7 +83,7 @@ def test_prefix_prefill_matches_oracle(cuda_ok, name):
     kv_len = [s + n_new for s in starts]
     layer = layers - 1
     q = torch.randn(batch, n_new, hq, 128, generator=gen, device="cuda").to(torch.bfloat16)
-    maps = prefill_kv_maps(vas, kv_len, st.geo)
+    maps = kv_tensor_maps(vas, kv_len, st.geo)
     start_t = torch.tensor(starts, dtype=torch.int32, device="cuda")
     out = prefill_attention(q, maps, start_t, layer, st.geo)
     torch.cuda.synchronize()
