@@ -278,26 +278,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
-          // Log-sum-exp merge with all loads in flight at once: lane k<S*G
-          // fetches (m, l) of one (split, head); weights are shuffled out.
+          // Log-sum-exp merge; loads are independent so they overlap (MLP).
           const int64_t u0 = bh * a.n_splits;
           const int S = w.splits_b;
-          float mk = -INFINITY, lk = 0.f;
-          if (lane < S * G) {
-            const int k = lane / G, c = lane % G;
-            mk = __ldcg(&a.part_ml[((u0 + k) * G + c) * 2]);
-            lk = __ldcg(&a.part_ml[((u0 + k) * G + c) * 2 + 1]);
-          }
           for (int c = 0; c < G; ++c) {
-            float mx = -INFINITY;
-            for (int k = 0; k < S; ++k) mx = fmaxf(mx, __shfl_sync(0xffffffffu, mk, k * G + c));
-            float den = 0.f;
+            const float* pm = a.part_ml + (u0 * G + c) * 2;  // stride G*2 per split
+            float mloc = -INFINITY;
+            for (int k = lane; k < S; k += 32) mloc = fmaxf(mloc, __ldcg(pm + k * G * 2));
+            const float mx = warp_max(mloc);
+            float dloc = 0.f;
+            for (int k = lane; k < S; k += 32)
+              dloc += tc::ex2(__ldcg(pm + k * G * 2) - mx) * __ldcg(pm + k * G * 2 + 1);
+            const float den = warp_sum(dloc);
             float acc[D / 32];
 #pragma unroll
             for (int j = 0; j < D / 32; ++j) acc[j] = 0.f;
+#pragma unroll 4
             for (int k = 0; k < S; ++k) {
-              const float wgt = tc::ex2(__shfl_sync(0xffffffffu, mk, k * G + c) - mx);
-              den += wgt * __shfl_sync(0xffffffffu, lk, k * G + c);
+              const float wgt = tc::ex2(__ldcg(pm + k * G * 2) - mx);
               const float* po = a.part_o + ((u0 + k) * G + c) * D + lane;
 #pragma unroll
               for (int j = 0; j < D / 32; ++j) acc[j] = fmaf(wgt, __ldcg(po + 32 * j), acc[j]);
@@ -463,7 +461,7 @@ int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
                         int32_t n_splits, int32_t split, float scale, void* out, float* part_o,
                         float* part_ml, int32_t* arrivals, int32_t n_sms, cudaStream_t stream) {
   const int G = g->q_heads / g->kv_heads;
-  if (G > MAXG || split % TILE || n_splits * G > 32) return cudaErrorInvalidValue;
+  if (G > MAXG || split % TILE) return cudaErrorInvalidValue;
   static_assert(sizeof(Smem) + 1024 <= 232448, "shared memory budget");
   CUtensorMap qmap;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D),
