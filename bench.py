@@ -204,8 +204,10 @@ class DecodeWorkload:
         self.geo = KVGeometry.from_config(self.cfg, hq)
         tpc = self.cfg.tokens_per_chunk
         self.rids = [f"r{b}" for b in range(B)]
-        # staggered lengths: ctx-15 .. ctx so chunk boundaries are crossed every step
-        self.lens = [ctx - (tpc - 1) + (b % tpc) if ctx >= tpc else ctx for b in range(B)]
+        # staggered lengths over one map-ahead window (4 chunks): every step some
+        # request runs out of headroom and extends by a 4-chunk run
+        win = 4 * tpc
+        self.lens = [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx for b in range(B)]
         gen = torch.Generator(device="cuda").manual_seed(seed)
         vas = []
         for rid, n in zip(self.rids, self.lens):
@@ -235,18 +237,55 @@ class DecodeWorkload:
         self.last_done = None
         self.extend_ns: list[int] = []
         self.chunks_mapped = 0
-        self._issue_extends()  # capacity for the first step's token
+        self.extend_calls = 0
+        self.map_ahead = 4         # chunks mapped per extend: one cuMemSetAccess per run
+        self.chunk_ticket: dict[tuple[int, int], int] = {}
+        self._prewarm(1024)
+        # staggered initial headroom (0..63 tokens past the next token) so the
+        # map-ahead extends are spread evenly over the steps that follow
+        for b, rid in enumerate(self.rids):
+            self.sched.extend(rid, min(self.max_seq, self.lens[b] + 1 + (b * win) // B))
+        self.dev.wait()
         torch.cuda.synchronize()
 
     # -- manager half ---------------------------------------------------------
+    def _prewarm(self, chunks: int):
+        """Warm the pSet free list (lazy deallocation, ops.py:150-178): admit and
+        release placeholder requests so steady-state extends reuse parked chunks
+        instead of paying cuMemCreate under load."""
+        tpc = self.cfg.tokens_per_chunk
+        per = self.max_seq // tpc
+        i = 0
+        while chunks > 0:
+            n = min(per, chunks)
+            self.sched.create(f"prewarm{i}", [0] * (n * tpc))
+            self.sched.release(f"prewarm{i}")
+            chunks -= n
+            i += 1
+        self.dev.wait()
+
     def _issue_extends(self):
-        t0 = time.perf_counter_ns()
-        n = 0
-        for rid, length in zip(self.rids, self.host_lens):
-            n += self.sched.extend(rid, length + 1)
-        if n:
-            self.extend_ns.append((time.perf_counter_ns() - t0) // n)
-        self.chunks_mapped += n
+        """VTS extend with map-ahead: when a request has less than one chunk of
+        headroom past its next token, extend by `map_ahead` chunks (one
+        contiguous run -> one cuMemSetAccess). Each newly mapped chunk records
+        the worker ticket that makes it valid; a launch waits only for the
+        chunks it touches, which were issued steps earlier."""
+        tpc = self.cfg.tokens_per_chunk
+        for b, (rid, length) in enumerate(zip(self.rids, self.host_lens)):
+            space = self.sched.mem[rid].vt.space
+            if space.mapped_pages * tpc >= length + 1 + tpc:
+                continue
+            first = space.mapped_pages
+            target = min(self.max_seq, length + 1 + self.map_ahead * tpc)
+            t0 = time.perf_counter_ns()
+            n = self.sched.extend(rid, target)
+            if n:
+                self.extend_ns.append(time.perf_counter_ns() - t0)
+                self.extend_calls += 1
+                tk = self.dev.ticket()
+                for c in range(first, first + n):
+                    self.chunk_ticket[(b, c)] = tk
+            self.chunks_mapped += n
 
     def algorithmic_bytes_per_step(self) -> int:
         """KV read (all layers, len+1 tokens incl. the new one) + q + out + appended K/V."""
@@ -269,17 +308,21 @@ class DecodeWorkload:
         k_new = self.k_new if k_new is None else k_new
         v_new = self.v_new if v_new is None else v_new
         out = self.out if out is None else out
-        ticket = self.dev.ticket()
-        if not self.dev.ready(ticket):
+        tpc = self.cfg.tokens_per_chunk
+        # the only pages this step touches: the chunk of each request's new token
+        ticket = max(self.chunk_ticket.pop((b, n // tpc), 0) if n % tpc == 0 else 0
+                     for b, n in enumerate(self.host_lens))
+        if ticket and not self.dev.ready(ticket):
             self.host_waits += 1
             if self.last_done is not None and self.last_done.query():
                 self.stalls += 1  # GPU drained while this step's pages were still mapping
-        self.dev.wait(ticket)
+        if ticket:
+            self.dev.wait(ticket)
         kv_maps = None
-        if self.maps is not None:  # TMA descriptors follow the newly mapped chunks
-            tpc = self.cfg.tokens_per_chunk
-            kv_maps = self.maps.update(
-                self.vas, [self.sched.mem[r].vt.space.mapped_pages * tpc for r in self.rids])
+        if self.maps is not None:
+            # TMA chunk extent = chunks holding valid tokens (all waited for):
+            # chunks mapped ahead may still be in flight on the worker
+            kv_maps = self.maps.update(self.vas, [-(-(n + 1) // tpc) * tpc for n in self.host_lens])
         kv_append(k_new, v_new, self.kv_va, self.seq, self.geo)
         self.seq.add_(1)
         mx = max(self.host_lens) + 1
@@ -446,6 +489,8 @@ def run_ours(args, world, rank, local):
             },
             "extend": {
                 "chunks_mapped": wl.chunks_mapped - mapped0,
+                "extend_calls": len(wl.extend_ns),
+                "chunks_per_extend": wl.map_ahead,
                 "host_submit_us_p50": round(ext[len(ext) // 2] / 1e3, 2),
                 "host_submit_us_p99": round(ext[min(len(ext) - 1, int(len(ext) * 0.99))] / 1e3, 2),
                 "driver_map_us_mean": round(drv["map_ns_total"] / max(drv["map_calls"], 1) / 1e3, 2),

@@ -25,6 +25,8 @@
 // unit never reads unmapped VA. Stale rows of a partial
 // stage are masked to -inf in the scores and skipped in PV.
 
+#include <algorithm>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -382,6 +384,25 @@ static thread_local int32_t g_last_launches = 0;
 
 extern "C" int32_t vt_attn_last_launches(void) { return g_last_launches; }
 
+// Persistent tcgen05 kernel: pick the split count that minimises the makespan
+// in 128-token tiles, ceil(units / SMs) * (tiles per unit + 1 unit overhead),
+// then spread max_seq_len evenly over that many splits (multiple of 128).
+static int tc_split(int32_t batch, int32_t hkv, int32_t max_seq_len, int n_sms) {
+  int best = 1;
+  long best_cost = -1;
+  for (int ns = 1; ns <= 16; ++ns) {
+    const long units = static_cast<long>(batch) * hkv * ns;
+    const long per_sm = (units + n_sms - 1) / n_sms;
+    const long tiles = (((max_seq_len + ns - 1) / ns) + 127) / 128;
+    const long cost = per_sm * (tiles + 1);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = ns;
+    }
+  }
+  return (((max_seq_len + best - 1) / best) + 127) / 128 * 128;
+}
+
 static int default_split(int32_t max_seq_len, bool tcgen05) {
   // tcgen05 (persistent): long units amortise the per-unit prologue; >= 2
   // splits per (request, kv head) keep ~7 units per SM at batch 64.
@@ -396,8 +417,10 @@ static size_t counters_bytes(int32_t batch, int32_t hkv) {
 
 extern "C" size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t batch,
                                             int32_t max_seq_len, int32_t split_tokens) {
-  // sized for the smaller default split so one workspace serves both paths
-  const int split = split_tokens > 0 ? split_tokens : default_split(max_seq_len, false);
+  // sized for the smallest split either path may pick (tc_split >= 128 tokens per
+  // split only when it needs <= 16 splits; CUDA-core default >= 512)
+  const int split = split_tokens > 0 ? split_tokens : std::min(default_split(max_seq_len, false),
+                                                               (max_seq_len + 15) / 16);
   const int64_t n_splits = (max_seq_len + split - 1) / split;
   const int64_t units = static_cast<int64_t>(batch) * g->kv_heads * n_splits;
   const int64_t G = g->q_heads / g->kv_heads;
@@ -428,8 +451,10 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
   g_last_launches = 0;
   if (g->head_dim != kD || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
   const int G = g->q_heads / g->kv_heads;
-  const int split =
-      split_tokens > 0 ? split_tokens : default_split(max_seq_len, kv_maps != nullptr);
+  const bool tc = kv_maps != nullptr && batch <= 1024;
+  const int split = split_tokens > 0 ? split_tokens
+                    : tc             ? tc_split(batch, g->kv_heads, max_seq_len, num_sms())
+                                     : default_split(max_seq_len, false);
   if (split % kStageTok) return cudaErrorInvalidValue;
   if (batch <= 0 || max_seq_len <= 0) return 0;
   const int n_splits = (max_seq_len + split - 1) / split;
@@ -458,7 +483,7 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   dim3 grid(n_splits, g->kv_heads, batch);
   cudaError_t e;
-  if (kv_maps != nullptr && batch <= 1024) {  // tcgen05 path (TMA maps over the request VAs)
+  if (tc) {  // tcgen05 path (TMA maps over the request VAs)
     int rc = vt_launch_decode_tc(g, layer, q, kv_maps, seq_lens, batch, n_splits, split, scale,
                                  out, a.part_o, a.part_ml, arrivals, num_sms(), st);
     g_last_launches = 1;

@@ -87,9 +87,12 @@ struct Unit {
   int b, h, s, t0, t1, splits_b;
 };
 
+// Split-major unit order: the CTA striding u, u+grid, ... gets a mix of long
+// (first) and short (last) splits of a request instead of always the same split.
 __device__ __forceinline__ bool unit_of(const Args& a, const int32_t* lens, int u, Unit& w) {
-  w.s = u % a.n_splits;
-  const int bh = u / a.n_splits;
+  const int nbh = a.batch * a.hkv;
+  w.s = u / nbh;
+  const int bh = u % nbh;
   w.h = bh % a.hkv;
   w.b = bh / a.hkv;
   const int len = lens[w.b];
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!unit_of(a, sm.lens, u, w)) continue;
         const CUtensorMap* kvmap = a.kv + w.b;
         if (u + static_cast<int>(gridDim.x) < n_units)  // warm the next unit's descriptor
-          tma_prefetch_desc(a.kv + (u + gridDim.x) / (a.n_splits * a.hkv));
+          tma_prefetch_desc(a.kv + ((u + gridDim.x) % (a.batch * a.hkv)) / a.hkv);
         const int qb = qc & 1;
         if (qc >= 2) mbar_wait(&sm.q_empty[qb], ((qc >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.q_full[qb], 2 * NQ * 64 * 2);
