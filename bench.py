@@ -437,9 +437,9 @@ def run_ours(args, world, rank, local):
     per_launch_s = kern_ms * 1e-3 / n_decode
     achieved = (decode_bytes / n_decode) / per_launch_s / 1e9
     traffic = None
-    try:
+    try:  # from the committed ncu --set full capture of this kernel (per launch)
         prof = json.load(open(os.path.join(REPO, "profiles", "decode_traffic.json")))
-        traffic = prof.get("dram_bytes_per_launch")
+        traffic = prof[args.path]["dram_bytes_per_launch"]
     except Exception:
         pass
 
