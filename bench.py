@@ -50,10 +50,12 @@ MIB = 1 << 20
 GIB = 1 << 30
 
 CONFIGS = {
-    # name: (layers, kv_heads, q_heads, batch_per_gpu, ctx)
-    "llama3-8b-decode": (32, 8, 32, 64, 4096),
-    "toy-cfg1": (1, 8, 8, 8, 4096),
+    # name: (layers, kv_heads, q_heads, batch_per_gpu_or_total, ctx)
+    "llama3-8b-decode": (32, 8, 32, 64, 4096),   # config 2 (request partition)
+    "llama2-70b-decode": (80, 8, 64, 64, 4096),  # config 4 (kv-head partition)
+    "toy-cfg1": (1, 8, 8, 8, 4096),              # config 1 shape
 }
+HEAD_PARTITIONED = {"llama2-70b-decode"}
 
 
 def parse():
@@ -177,91 +179,122 @@ def sum_over_ranks(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------- the workload --
-class DecodeWorkload:
-    """64 requests of one GPU, their vTensor spaces, and the per-step driver."""
+class _Group:
+    """One layer group: its own manager (pool/VTO/VTS) on the GPU's shared VMM
+    device, geometry (layers_in_group, local kv heads), KV-map cache."""
 
-    def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05"):
+    def __init__(self, wl, first_layer, geom, seed):
         import torch
 
         import paper_2407_15309_b200 as vt
-        from paper_2407_15309_b200.attention import DecodeWorkspace, KVMapCache
+        from paper_2407_15309_b200.attention import KVMapCache
         from paper_2407_15309_b200.kv_layout import KVGeometry, chunk_view
 
-        L, hkv, hq, B, ctx = CONFIGS[cfg_name]
-        self.L, self.hkv, self.hq, self.B, self.ctx = L, hkv, hq, B, ctx
-        self.max_seq = ctx + 1024
+        self.first = first_layer
+        self.n_layers = geom.layers
         self.cfg = vt.SimConfig(
-            capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB, weights_bytes=0,
-            geometry=vt.ModelGeometry(layers=L, kv_heads=hkv, head_dim=128, elem_bytes=2),
-            max_seq_len=self.max_seq, initial_alloc_tokens=0, lookahead_chunks=1, max_batch=B)
-        self.dev = vt.VirtualMemoryDevice(
-            vt.DeviceConfig(capacity_bytes=self.cfg.capacity_bytes,
-                            chunk_size_bytes=self.cfg.chunk_size_bytes),
-            cuda_ordinal=torch.cuda.current_device())
+            capacity_bytes=wl.dev.config.capacity_bytes, chunk_size_bytes=2 * MIB,
+            weights_bytes=0, geometry=geom, max_seq_len=wl.max_seq, initial_alloc_tokens=0,
+            lookahead_chunks=1, max_batch=wl.B)
         self.pool = vt.TensorPool(self.cfg.tokens_per_chunk)
-        self.ops = vt.VTensorOps(self.dev, self.pool, self.cfg)
+        self.ops = vt.VTensorOps(wl.dev, self.pool, self.cfg)
         self.sched = vt.VTensorScheduler(self.ops)
-        self.geo = KVGeometry.from_config(self.cfg, hq)
-        tpc = self.cfg.tokens_per_chunk
-        self.rids = [f"r{b}" for b in range(B)]
-        # staggered lengths over one map-ahead window (4 chunks): every step some
-        # request runs out of headroom and extends by a 4-chunk run
-        win = 4 * tpc
-        self.lens = [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx for b in range(B)]
+        self.geo = KVGeometry.from_config(self.cfg, wl.hq)
+        self.tpc = self.cfg.tokens_per_chunk
         gen = torch.Generator(device="cuda").manual_seed(seed)
-        vas = []
-        for rid, n in zip(self.rids, self.lens):
+        self.vas = []
+        for rid, n in zip(wl.rids, wl.lens):
             self.sched.create(rid, [1] * n)
             self.sched.mark_prefilled(rid)
-            vas.append(self.dev.va(self.sched.mem[rid].vt.space.rng))
-        self.dev.wait()
-        for va, rid in zip(vas, self.rids):
-            pages = self.sched.mem[rid].vt.space.mapped_pages
-            view = chunk_view(va, pages, self.geo)
+            self.vas.append(wl.dev.va(self.sched.mem[rid].vt.space.rng))
+        wl.dev.wait()
+        for va, rid in zip(self.vas, wl.rids):
+            view = chunk_view(va, self.sched.mem[rid].vt.space.mapped_pages, self.geo)
             view.copy_(torch.randn(view.shape, generator=gen, device="cuda").to(torch.bfloat16))
-        self.kv_va = torch.tensor(vas, dtype=torch.int64, device="cuda")
-        self.seq = torch.tensor(self.lens, dtype=torch.int32, device="cuda")
+        self.kv_va = torch.tensor(self.vas, dtype=torch.int64, device="cuda")
+        self.maps = KVMapCache(self.geo, wl.B) if wl.path == "tcgen05" else None
+        self.chunk_ticket: dict[tuple[int, int], int] = {}
+
+
+class DecodeWorkload:
+    """The requests one GPU serves, their vTensor spaces, and the step driver.
+
+    Request partition (default configs): every rank serves its own `B`
+    requests. KV-head partition (llama2-70b-decode): every rank serves all `B`
+    requests for its slice of kv / q heads. Models whose per-token KV does not
+    divide a 2 MiB chunk are managed as layer groups (sharding.layer_groups).
+    """
+
+    def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05",
+                 world: int = 1, rank: int = 0):
+        import torch
+
+        import paper_2407_15309_b200 as vt
+        from paper_2407_15309_b200.attention import DecodeWorkspace
+        from paper_2407_15309_b200.sharding import head_shard, layer_groups
+
+        L, hkv, hq, B, ctx = CONFIGS[cfg_name]
+        self.head_partition = cfg_name in HEAD_PARTITIONED
+        if self.head_partition:
+            sh = head_shard(hkv, hq, world, rank)
+            hkv, hq = sh.local_kv_heads, sh.local_q_heads
+        self.L, self.hkv, self.hq, self.B, self.ctx = L, hkv, hq, B, ctx
+        self.path = path
+        self.max_seq = ctx + 1024
+        self.dev = vt.VirtualMemoryDevice(
+            vt.DeviceConfig(capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB),
+            cuda_ordinal=torch.cuda.current_device())
+        groups = layer_groups(L, hkv)
+        tpc = 2 * MIB // groups[0][1].bytes_per_token
+        self.map_ahead = 4         # chunks mapped per extend: one cuMemSetAccess per run
+        win = self.map_ahead * tpc
+        self.rids = [f"r{b}" for b in range(B)]
+        # staggered lengths over one map-ahead window: every step some request
+        # runs out of headroom and extends by a `map_ahead`-chunk run
+        self.lens = [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx for b in range(B)]
+        self.groups = [_Group(self, first, geom, seed + 17 * i)
+                       for i, (first, geom) in enumerate(groups)]
+        gen = torch.Generator(device="cuda").manual_seed(seed)
         self.q = torch.randn(L, B, hq, 128, generator=gen, device="cuda").to(torch.bfloat16)
         self.k_new = torch.randn(L, B, hkv, 128, generator=gen, device="cuda").to(torch.bfloat16)
         self.v_new = torch.randn_like(self.k_new)
         self.out = torch.empty_like(self.q)
         self.split = split
-        self.path = path
-        self.ws = DecodeWorkspace(self.geo, B, self.max_seq, split)
-        self.vas = vas
-        self.maps = KVMapCache(self.geo, B) if path == "tcgen05" else None
+        self.ws = DecodeWorkspace(self.groups[0].geo, B, self.max_seq, split)
         self.stream = torch.cuda.current_stream()
+        self.seq = torch.tensor(self.lens, dtype=torch.int32, device="cuda")
+        self.seq1 = torch.empty_like(self.seq)
         self.host_lens = list(self.lens)
         self.stalls = 0
         self.host_waits = 0
         self.last_done = None
         self.extend_ns: list[int] = []
         self.chunks_mapped = 0
-        self.extend_calls = 0
-        self.map_ahead = 4         # chunks mapped per extend: one cuMemSetAccess per run
-        self.chunk_ticket: dict[tuple[int, int], int] = {}
         self._prewarm(1024)
-        # staggered initial headroom (0..63 tokens past the next token) so the
-        # map-ahead extends are spread evenly over the steps that follow
-        for b, rid in enumerate(self.rids):
-            self.sched.extend(rid, min(self.max_seq, self.lens[b] + 1 + (b * win) // B))
+        for grp in self.groups:  # staggered initial headroom (0..win-1 tokens)
+            for b, rid in enumerate(self.rids):
+                grp.sched.extend(rid, min(self.max_seq, self.lens[b] + 1 + (b * win) // B))
         self.dev.wait()
         torch.cuda.synchronize()
 
+    @property
+    def kv_bytes_per_token(self) -> int:
+        return self.L * 2 * self.hkv * 128 * 2
+
     # -- manager half ---------------------------------------------------------
     def _prewarm(self, chunks: int):
-        """Warm the pSet free list (lazy deallocation, ops.py:150-178): admit and
-        release placeholder requests so steady-state extends reuse parked chunks
-        instead of paying cuMemCreate under load."""
-        tpc = self.cfg.tokens_per_chunk
-        per = self.max_seq // tpc
-        i = 0
-        while chunks > 0:
-            n = min(per, chunks)
-            self.sched.create(f"prewarm{i}", [0] * (n * tpc))
-            self.sched.release(f"prewarm{i}")
-            chunks -= n
-            i += 1
+        """Warm each group's pSet free list (lazy deallocation, ops.py:150-178):
+        admit and release placeholder requests so steady-state extends reuse
+        parked chunks instead of paying cuMemCreate under load."""
+        for grp in self.groups:
+            per = self.max_seq // grp.tpc
+            left, i = chunks // len(self.groups), 0
+            while left > 0:
+                n = min(per, left)
+                grp.sched.create(f"prewarm{i}", [0] * (n * grp.tpc))
+                grp.sched.release(f"prewarm{i}")
+                left -= n
+                i += 1
         self.dev.wait()
 
     def _issue_extends(self):
@@ -270,29 +303,27 @@ class DecodeWorkload:
         contiguous run -> one cuMemSetAccess). Each newly mapped chunk records
         the worker ticket that makes it valid; a launch waits only for the
         chunks it touches, which were issued steps earlier."""
-        tpc = self.cfg.tokens_per_chunk
-        for b, (rid, length) in enumerate(zip(self.rids, self.host_lens)):
-            space = self.sched.mem[rid].vt.space
-            if space.mapped_pages * tpc >= length + 1 + tpc:
-                continue
-            first = space.mapped_pages
-            target = min(self.max_seq, length + 1 + self.map_ahead * tpc)
-            t0 = time.perf_counter_ns()
-            n = self.sched.extend(rid, target)
-            if n:
-                self.extend_ns.append(time.perf_counter_ns() - t0)
-                self.extend_calls += 1
-                tk = self.dev.ticket()
-                for c in range(first, first + n):
-                    self.chunk_ticket[(b, c)] = tk
-            self.chunks_mapped += n
+        for grp in self.groups:
+            tpc = grp.tpc
+            for b, (rid, length) in enumerate(zip(self.rids, self.host_lens)):
+                space = grp.sched.mem[rid].vt.space
+                if space.mapped_pages * tpc >= length + 1 + tpc:
+                    continue
+                first = space.mapped_pages
+                target = min(self.max_seq, length + 1 + self.map_ahead * tpc)
+                t0 = time.perf_counter_ns()
+                n = grp.sched.extend(rid, target)
+                if n:
+                    self.extend_ns.append(time.perf_counter_ns() - t0)
+                    tk = self.dev.ticket()
+                    for c in range(first, first + n):
+                        grp.chunk_ticket[(b, c)] = tk
+                self.chunks_mapped += n
 
     def algorithmic_bytes_per_step(self) -> int:
         """KV read (all layers, len+1 tokens incl. the new one) + q + out + appended K/V."""
-        kv = sum(2 * (n + 1) * self.hkv * 128 * 2 for n in self.host_lens) * self.L
-        qo = 2 * self.q.numel() * 2
-        app = 2 * self.k_new.numel() * 2
-        return kv + qo + app
+        kv = sum(n + 1 for n in self.host_lens) * self.kv_bytes_per_token
+        return kv + 2 * self.q.numel() * 2 + 2 * self.k_new.numel() * 2
 
     def decode_bytes_per_launch(self) -> int:
         return (sum(2 * (n + 1) * self.hkv * 128 * 2 for n in self.host_lens)
@@ -308,48 +339,59 @@ class DecodeWorkload:
         k_new = self.k_new if k_new is None else k_new
         v_new = self.v_new if v_new is None else v_new
         out = self.out if out is None else out
-        tpc = self.cfg.tokens_per_chunk
         # the only pages this step touches: the chunk of each request's new token
-        ticket = max(self.chunk_ticket.pop((b, n // tpc), 0) if n % tpc == 0 else 0
-                     for b, n in enumerate(self.host_lens))
+        ticket = 0
+        for grp in self.groups:
+            for b, n in enumerate(self.host_lens):
+                if n % grp.tpc == 0:
+                    ticket = max(ticket, grp.chunk_ticket.pop((b, n // grp.tpc), 0))
         if ticket and not self.dev.ready(ticket):
             self.host_waits += 1
             if self.last_done is not None and self.last_done.query():
                 self.stalls += 1  # GPU drained while this step's pages were still mapping
         if ticket:
             self.dev.wait(ticket)
-        kv_maps = None
-        if self.maps is not None:
-            # TMA chunk extent = chunks holding valid tokens (all waited for):
-            # chunks mapped ahead may still be in flight on the worker
-            kv_maps = self.maps.update(self.vas, [-(-(n + 1) // tpc) * tpc for n in self.host_lens])
-        kv_append(k_new, v_new, self.kv_va, self.seq, self.geo)
-        self.seq.add_(1)
         mx = max(self.host_lens) + 1
         launches = 1
-        for layer in range(self.L):
-            if layer_events is not None:
-                layer_events[layer][0].record(self.stream)
-            decode_attention(q[layer], self.kv_va, self.seq, layer, self.geo, mx,
-                             out=out[layer], workspace=self.ws, split_tokens=self.split,
-                             kv_maps=kv_maps)
-            if layer_events is not None:
-                layer_events[layer][1].record(self.stream)
-            launches += last_launches()
+        torch.add(self.seq, 1, out=self.seq1)  # lengths including this step's token
+        for grp in self.groups:
+            kv_maps = None
+            if grp.maps is not None:
+                # TMA chunk extent = chunks holding valid tokens (all waited
+                # for); chunks mapped ahead may still be in flight on the worker
+                kv_maps = grp.maps.update(
+                    grp.vas, [-(-(n + 1) // grp.tpc) * grp.tpc for n in self.host_lens])
+            lo = grp.first
+            kv_append(k_new[lo:lo + grp.n_layers], v_new[lo:lo + grp.n_layers], grp.kv_va,
+                      self.seq, grp.geo)
+            launches += 1
+            for li in range(grp.n_layers):
+                layer = lo + li
+                if layer_events is not None:
+                    layer_events[layer][0].record(self.stream)
+                decode_attention(q[layer], grp.kv_va, self.seq1, li, grp.geo, mx,
+                                 out=out[layer], workspace=self.ws, split_tokens=self.split,
+                                 kv_maps=kv_maps)
+                if layer_events is not None:
+                    layer_events[layer][1].record(self.stream)
+                launches += last_launches()
+        self.seq, self.seq1 = self.seq1, self.seq
         self.dev.fence(self.stream.cuda_stream)
         self.last_done = torch.cuda.Event()
         self.last_done.record(self.stream)
-        for rid in self.rids:
-            self.sched.append_token(rid, 1)
+        for grp in self.groups:
+            for rid in self.rids:
+                grp.sched.append_token(rid, 1)
         self.host_lens = [n + 1 for n in self.host_lens]
-        self._issue_extends()  # next step's pages: overlap with this step's kernels
+        self._issue_extends()  # next steps' pages: overlap with this step's kernels
         return launches
 
 
 def run_ours(args, world, rank, local):
     import torch
 
-    wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path)
+    wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
+                        world=world, rank=rank)
     if args.profile_steps:
         for _ in range(args.profile_steps):
             wl.step()
@@ -392,7 +434,7 @@ def run_ours(args, world, rank, local):
     stalls = wl.stalls - stalls0
     elapsed_max = max_over_ranks(elapsed_ms, world)
     bytes_all = sum_over_ranks(bytes_total, world)
-    tokens_all = wl.B * args.steps * world
+    tokens_all = wl.B * args.steps * (1 if wl.head_partition else world)
     value = bytes_all / (elapsed_max * 1e-3) / 1e9
 
     # ---- e2e: host buffers through the public API ----
@@ -458,17 +500,19 @@ def run_ours(args, world, rank, local):
             "warmup": args.warmup,
             "ms_per_step": round(elapsed_max / args.steps, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if wl.head_partition else "weak",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (seeded randn bf16 KV in real cuMemMap'd 2 MiB chunks)",
             "config": {
                 "workload": f"{args.config}: decode step, {wl.L} layers, {wl.hq} q / {wl.hkv} kv "
-                            f"heads, d 128, batch {wl.B}/GPU, ctx {min(wl.lens)}..{max(wl.lens)}",
+                            f"heads per GPU, d 128, batch {wl.B}, ctx {min(wl.lens)}..{max(wl.lens)}",
                 "batch_per_gpu": wl.B, "context": wl.ctx, "layers": wl.L,
-                "parallelism": f"request-partition x{world} (no collective)",
+                "parallelism": (f"kv-head partition x{world} (no collective)" if wl.head_partition
+                                else f"request partition x{world} (no collective)"),
+                "layer_groups": len(wl.groups),
                 "l2": "inputs larger than L2 (KV working set %.1f GiB)" % (
-                    sum(wl.host_lens) * wl.cfg.bytes_per_token / GIB),
+                    sum(wl.host_lens) * wl.kv_bytes_per_token / GIB),
                 "split_tokens": args.split or "auto",
                 "decode_path": args.path,
             },

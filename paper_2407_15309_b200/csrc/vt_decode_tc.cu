@@ -102,6 +102,38 @@ __device__ __forceinline__ bool unit_of(const Args& a, const int32_t* lens, int 
   return w.t0 < w.t1;
 }
 
+// Column max of G scores across the 32 lanes of a warp by exchange-halving:
+// each step trades half of the remaining columns with the partner lane, so
+// G=8 costs 9 shuffles instead of 40. Returns the max of column `col`.
+template <int G>
+__device__ __forceinline__ float warp_colmax(float (&v)[G], int lane, int& col) {
+  int n = G;
+  int own = 0;
+#pragma unroll
+  for (int bit = 4; bit >= 0; --bit) {
+    const int m = 1 << bit;
+    if (n > 1) {
+      const int half = n >> 1;
+      const bool up = (lane >> bit) & 1;
+#pragma unroll
+      for (int i = 0; i < G / 2; ++i) {
+        if (i < half) {
+          const float send = up ? v[i] : v[i + half];
+          const float keep = up ? v[i + half] : v[i];
+          v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, m));
+        }
+      }
+      own += up ? half : 0;
+      n = half;
+    } else {
+      v[0] = fmaxf(v[0], __shfl_xor_sync(0xffffffffu, v[0], m));
+    }
+  }
+  col = own;
+  return v[0];
+}
+
+template <int G>
 __global__ void __launch_bounds__(kThreads, 1)
     decode_tc_kernel(const __grid_constant__ CUtensorMap q_map, const Args a) {
   extern __shared__ uint8_t smem_raw[];
@@ -110,7 +142,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_units = a.batch * a.hkv * a.n_splits;
-  const int G = a.group;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < KSTAGES; ++i) {
@@ -331,9 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      float m_run[NQ], l_thr[NQ], o_acc[NQ], alpha_prev[NQ];
+      float m_run[G], l_thr[G], o_acc[G], alpha_prev[G];
 #pragma unroll
-      for (int c = 0; c < NQ; ++c) {
+      for (int c = 0; c < G; ++c) {
         m_run[c] = -INFINITY;
         l_thr[c] = 0.f;
         o_acc[c] = 0.f;
@@ -349,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::ld16(lane_addr + kOCol + (gt & 1) * NQ, o);
         tc::wait_ld();
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) o_acc[c] = fmaf(o_acc[c], alpha_prev[c], __uint_as_float(o[c]));
+        for (int c = 0; c < G; ++c) o_acc[c] = fmaf(o_acc[c], alpha_prev[c], __uint_as_float(o[c]));
       };
       const int g_first = g;
       for (int tok0 = w.t0; tok0 < w.t1; tok0 += TILE, ++g) {
@@ -359,39 +390,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::ld16(lane_addr + kSCol + (g & 1) * NQ, r);
         tc::wait_ld();
         const bool valid = tok0 + row < w.t1;
-        float x[NQ];
-        float mx[NQ];
+        float x[G];
+        float mx[G];
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) {
+        for (int c = 0; c < G; ++c) {
           x[c] = valid ? __uint_as_float(r[c]) * sl2 : -INFINITY;
           mx[c] = x[c];
         }
-#pragma unroll
-        for (int c = 0; c < NQ; ++c)
-          if (c < G) mx[c] = warp_max(mx[c]);
-        if (lane < NQ) {
-          float mine = mx[0];
-#pragma unroll
-          for (int c = 1; c < NQ; ++c)
-            if (lane == c) mine = mx[c];
-          sm.red[g & 1][quarter][lane] = mine;
+        {
+          int col;
+          const float cm = warp_colmax<G>(mx, lane, col);
+          if ((lane & ((32 / G) - 1)) == 0) sm.red[g & 1][quarter][col] = cm;
         }
         named_bar_sync(1, 128);
-        float alpha[NQ];
+        float alpha[G];
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) {
-          if (c < G) {
-            const float(*rd)[NQ] = sm.red[g & 1];
-            const float tmax = fmaxf(fmaxf(rd[0][c], rd[1][c]), fmaxf(rd[2][c], rd[3][c]));
-            const float m_new = fmaxf(m_run[c], tmax);
-            alpha[c] = tc::ex2(m_run[c] - m_new);
-            m_run[c] = m_new;
-            const float p = tc::ex2(x[c] - m_new);
-            x[c] = p;
-            l_thr[c] = l_thr[c] * alpha[c] + p;
-          } else {
-            alpha[c] = 1.f;
-          }
+        for (int c = 0; c < G; ++c) {
+          const float(*rd)[NQ] = sm.red[g & 1];
+          const float tmax = fmaxf(fmaxf(rd[0][c], rd[1][c]), fmaxf(rd[2][c], rd[3][c]));
+          const float m_new = fmaxf(m_run[c], tmax);
+          alpha[c] = tc::ex2(m_run[c] - m_new);
+          m_run[c] = m_new;
+          const float p = tc::ex2(x[c] - m_new);
+          x[c] = p;
+          l_thr[c] = l_thr[c] * alpha[c] + p;
         }
         if (tok0 + TILE > w.t1) {
           // tail tile: rows >= t1 may be stale bytes of the last mapped chunk
@@ -414,12 +436,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* blk = reinterpret_cast<uint8_t*>(sm.p[g & 1][row >> 6]);
           const int tk = row & 63;
 #pragma unroll
-          for (int c = 0; c < NQ; ++c) {
-            if (c < G) {
-              const int chunk = (tk >> 3) ^ (c & 7);
-              *reinterpret_cast<__nv_bfloat16*>(blk + c * 128 + (chunk << 4) + (tk & 7) * 2) =
-                  __float2bfloat16(x[c]);
-            }
+          for (int c = 0; c < G; ++c) {
+            const int chunk = (tk >> 3) ^ (c & 7);
+            *reinterpret_cast<__nv_bfloat16*>(blk + c * 128 + (chunk << 4) + (tk & 7) * 2) =
+                __float2bfloat16(x[c]);
           }
         }
         fence_proxy_async_smem();
@@ -427,20 +447,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&sm.p_full);
         if (g > g_first) fold(g - 1);
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) alpha_prev[c] = alpha[c];
+        for (int c = 0; c < G; ++c) alpha_prev[c] = alpha[c];
       }
       // ----- unit epilogue: hand (o, m, l) to the epilogue warp -----
       fold(g - 1);
       const int eb = uc & 1;
       if (uc >= 2) mbar_wait(&sm.epi_empty[eb], ((uc >> 1) & 1) ^ 1);
 #pragma unroll
-      for (int c = 0; c < MAXG; ++c) {
-        if (c < G) {
-          const float lw = warp_sum(l_thr[c]);
-          sm.epi[eb].o[c][row] = o_acc[c];
-          if (lane == 0) sm.epi[eb].lpart[quarter][c] = lw;
-          if (tid == 0) sm.epi[eb].m[c] = m_run[c];
-        }
+      for (int c = 0; c < G; ++c) {
+        const float lw = warp_sum(l_thr[c]);
+        sm.epi[eb].o[c][row] = o_acc[c];
+        if (lane == 0) sm.epi[eb].lpart[quarter][c] = lw;
+        if (tid == 0) sm.epi[eb].m[c] = m_run[c];
       }
       mbar_arrive(&sm.epi_full[eb]);
       ++uc;
@@ -490,14 +508,19 @@ int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
   a.layer = layer;
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t smem = sizeof(Smem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
   const int units = batch * g->kv_heads * n_splits;
   const int grid = units < n_sms ? units : n_sms;
-  decode_tc_kernel<<<grid, kThreads, smem, stream>>>(qmap, a);
+  auto launch = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    kernel<<<grid, kThreads, smem, stream>>>(qmap, a);
+  };
+  switch (G) {
+    case 1: launch(decode_tc_kernel<1>); break;
+    case 2: launch(decode_tc_kernel<2>); break;
+    case 4: launch(decode_tc_kernel<4>); break;
+    case 8: launch(decode_tc_kernel<8>); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }

@@ -71,7 +71,8 @@ def timed(fn, iters, warmup):
 
 
 def bench_decode(args, pk):
-    L, hkv, hq, B, ctx = 32, 8, 32, 64, 4096
+    # 8b: Llama-3-8B (G=4, tpc 16); 70b: one 16-layer group of Llama-2-70B (G=8, tpc 32)
+    L, hkv, hq, B, ctx = (32, 8, 32, 64, 4096) if args.shape == "8b" else (16, 8, 64, 64, 4096)
     cfg, dev, ops, sched, geo = stack(L, hkv, hq, ctx + 256, 20000)
     gen = torch.Generator(device="cuda").manual_seed(0)
     vas = []
@@ -111,7 +112,7 @@ def bench_decode(args, pk):
             nbytes = 2 * B * ctx * hkv * 128 * 2 + 2 * B * hq * 128 * 2
             gbs = nbytes / (ms * 1e-3) / 1e9
             res.append({"kernel": f"decode[{path}]" + ("x32" if args.loop else ""),
-                        "config": "cfg2 llama3-8b B64 ctx4096",
+                        "config": f"{args.shape} B64 ctx4096 G={hq // hkv}",
                         "split": split, "us": round(ms * 1e3, 2), "bytes": nbytes,
                         "GB/s": round(gbs, 1), "frac_of_hbm": round(gbs / pk["hbm_gbs"], 4)})
     dev.wait()
@@ -165,6 +166,7 @@ def main():
     ap.add_argument("--splits", type=lambda s: [int(x) for x in s.split(",")], default=[1024])
     ap.add_argument("--paths", type=lambda s: s.split(","), default=["tcgen05", "cuda_core"])
     ap.add_argument("--loop", action="store_true", help="time 32 back-to-back launches")
+    ap.add_argument("--shape", choices=["8b", "70b"], default="8b")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     pk = peaks()
