@@ -54,6 +54,7 @@ CONFIGS = {
     "llama3-8b-decode": (32, 8, 32, 64, 4096),   # config 2 (request partition)
     "llama2-70b-decode": (80, 8, 64, 64, 4096),  # config 4 (kv-head partition)
     "toy-cfg1": (1, 8, 8, 8, 4096),              # config 1 shape
+    "llama3-8b-32k": (32, 8, 32, 16, 32768 - 256),  # config 5: long context, batch 16
 }
 HEAD_PARTITIONED = {"llama2-70b-decode"}
 
@@ -70,6 +71,9 @@ def parse():
                     help="decode kernel: tcgen05/TMEM (default) or CUDA-core FFMA2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--premap", action="store_true",
+                    help="map every chunk the run will need up front (config-5 comparison)")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the config-3 prefill probe")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N untimed steps only (for ncu), print nothing")
     return ap.parse_args()
@@ -226,7 +230,7 @@ class DecodeWorkload:
     """
 
     def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05",
-                 world: int = 1, rank: int = 0):
+                 world: int = 1, rank: int = 0, premap_steps: int = 0):
         import torch
 
         import paper_2407_15309_b200 as vt
@@ -273,7 +277,8 @@ class DecodeWorkload:
         self._prewarm(1024)
         for grp in self.groups:  # staggered initial headroom (0..win-1 tokens)
             for b, rid in enumerate(self.rids):
-                grp.sched.extend(rid, min(self.max_seq, self.lens[b] + 1 + (b * win) // B))
+                extra = premap_steps + win if premap_steps else (b * win) // B
+                grp.sched.extend(rid, min(self.max_seq, self.lens[b] + 1 + extra))
         self.dev.wait()
         torch.cuda.synchronize()
 
@@ -390,8 +395,9 @@ class DecodeWorkload:
 def run_ours(args, world, rank, local):
     import torch
 
+    total_steps = args.warmup + 2 * args.steps + 2
     wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
-                        world=world, rank=rank)
+                        world=world, rank=rank, premap_steps=total_steps if args.premap else 0)
     if args.profile_steps:
         for _ in range(args.profile_steps):
             wl.step()
@@ -412,6 +418,7 @@ def run_ours(args, world, rank, local):
     stalls0 = wl.stalls
     waits0 = wl.host_waits
     drv0 = wl.dev.driver_stats()
+    wl.dev.driver_latencies("map_page", reset=True)
     wl.extend_ns.clear()
     mapped0 = wl.chunks_mapped
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -467,6 +474,7 @@ def run_ours(args, world, rank, local):
                "h2d_bytes_per_step": int((host_q.numel() + host_k.numel() + host_v.numel()) * 2),
                "d2h_bytes_per_step": int(host_o.numel() * 2)}
 
+    map_lat = sorted(wl.dev.driver_latencies("map_page")) or [0]
     drv_end = wl.dev.driver_stats()
     drv = {k: drv_end[k] - drv0[k] for k in drv_end}  # timed region only
     peaks = {}
@@ -488,6 +496,9 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, budget_s=8.0)
+    prefill = None
+    if rank == 0 and not args.no_prefill and args.config == "llama3-8b-decode":
+        prefill = prefill_probe()
 
     if rank == 0:
         ext = sorted(wl.extend_ns) or [0]
@@ -534,6 +545,9 @@ def run_ours(args, world, rank, local):
             "extend": {
                 "chunks_mapped": wl.chunks_mapped - mapped0,
                 "extend_calls": len(wl.extend_ns),
+                "ready_latency_us_p50": round(map_lat[len(map_lat) // 2] / 1e3, 1),
+                "ready_latency_us_p99": round(map_lat[min(len(map_lat) - 1, int(len(map_lat) * 0.99))] / 1e3, 1),
+                "ready_latency_note": "per mapped chunk, submit -> cuMemMap+cuMemSetAccess done on the worker",
                 "chunks_per_extend": wl.map_ahead,
                 "host_submit_us_p50": round(ext[len(ext) // 2] / 1e3, 2),
                 "host_submit_us_p99": round(ext[min(len(ext) - 1, int(len(ext) * 0.99))] / 1e3, 2),
@@ -547,11 +561,80 @@ def run_ours(args, world, rank, local):
             "gpu_launches": launches + 0,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "prefill_cfg3": prefill,
+            "premapped": bool(args.premap),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line))
     wl.dev.wait()
     torch.cuda.synchronize()
+
+
+# ------------------------------------------------------- config-3 prefill --
+def prefill_probe(iters: int = 8) -> dict:
+    """Config 3 through the manager: a 2048-token conversation is recorded in
+    the rTree, 16 follow-up turns prefix-match it (128 shared chunks mapped by
+    identity + 32 new chunks each), and the tcgen05 prefix-prefill kernel runs
+    the 512 new tokens of all 16 requests per layer (32 back-to-back layers)."""
+    import torch
+
+    import paper_2407_15309_b200 as vt
+    from paper_2407_15309_b200.attention import kv_tensor_maps, last_launches, prefill_attention
+    from paper_2407_15309_b200.kv_layout import KVGeometry, chunk_view
+
+    L, hkv, hq, B, prefix, n_new = 32, 8, 32, 16, 2048, 512
+    cfg = vt.SimConfig(capacity_bytes=16 * GIB, chunk_size_bytes=2 * MIB, weights_bytes=0,
+                       geometry=vt.ModelGeometry(L, hkv, 128, 2), max_seq_len=4096,
+                       initial_alloc_tokens=0)
+    dev = vt.VirtualMemoryDevice(vt.DeviceConfig(cfg.capacity_bytes, cfg.chunk_size_bytes),
+                                 cuda_ordinal=torch.cuda.current_device())
+    sched = vt.VTensorScheduler(vt.VTensorOps(dev, vt.TensorPool(cfg.tokens_per_chunk), cfg))
+    geo = KVGeometry.from_config(cfg, hq)
+    tpc = cfg.tokens_per_chunk
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    base = [i % 251 for i in range(prefix)]
+    sched.create("conv", base)
+    sched.mark_prefilled("conv")
+    dev.wait()
+    v = chunk_view(dev.va(sched.mem["conv"].vt.space.rng), prefix // tpc, geo)
+    v.copy_(torch.randn(v.shape, generator=gen, device="cuda").to(torch.bfloat16))
+    sched.prefix_record("conv")
+    vas, shared_ok = [], True
+    for b in range(B):
+        rm, st = sched.prefix_match(f"t{b}", base + [9000 + b * n_new + k for k in range(n_new)])
+        shared_ok &= st.identity_ok and st.shared_tokens == prefix
+        vas.append(dev.va(rm.vt.space.rng))
+    dev.wait()
+    for va in vas:
+        w = chunk_view(va, (prefix + n_new) // tpc, geo)[prefix // tpc:]
+        w.copy_(torch.randn(w.shape, generator=gen, device="cuda").to(torch.bfloat16))
+    maps = kv_tensor_maps(vas, [prefix + n_new] * B, geo)
+    start = torch.full((B,), prefix, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, n_new, hq, 128, generator=gen, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    for layer in range(3):
+        prefill_attention(q, maps, start, layer, geo, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(iters):
+        for layer in range(L):
+            prefill_attention(q, maps, start, layer, geo, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    per = e0.elapsed_time(e1) / (iters * L) * 1e-3
+    flops = 4 * hq * 128 * (n_new * prefix + n_new * (n_new + 1) // 2) * B
+    try:
+        pk = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pk = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+    tf = flops / per / 1e12
+    dev.wait()
+    return {"workload": "config 3: 16 x (2048 rTree-shared + 512 new), Llama-3-8B heads, per layer",
+            "prefix_shared_by_identity": bool(shared_ok), "us_per_layer": round(per * 1e6, 1),
+            "tflops": round(tf, 1), "frac_of_bf16_sustained": round(tf / pk["bf16_tflops_sustained"], 4),
+            "frac_of_bf16_burst": round(tf / pk["bf16_tflops"], 4),
+            "kernel": "vt::pf::prefill_kernel (tcgen05/TMEM/TMA)", "launches": last_launches()}
 
 
 # --------------------------------------------------------- CPU / reference --
@@ -590,7 +673,46 @@ def cpu_baseline(cfg_name: str, budget_s: float = 8.0) -> dict:
             "kind": "port",
             "sample": f"{nb} requests x 1 layer x {ctx} tokens ({hq}q/{hkv}kv heads), {reps} reps",
             "tokens_per_s_equiv": round(nb / (dt * L), 2),
+            "manager": manager_cpu_baseline(),
             "host_cpus": os.cpu_count(), "cpu_model": cpu_name}
+
+
+def manager_cpu_baseline() -> dict:
+    """vTensor extend / append on the host, 1 core: the reference's algorithm
+    (oracle/vtm_ref.py, reference cost model) vs this package's manager on the
+    simulated shim (same op stream, Llama-3-8B geometry, 64 requests at ~4k)."""
+    import paper_2407_15309_b200 as vt
+    from oracle import vtm_ref as R
+
+    out = {}
+    for name, ns in (("reference_port", R), ("ours_host_side", vt)):
+        cfg = ns.SimConfig(capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB, weights_bytes=0,
+                           geometry=ns.ModelGeometry(32, 8, 128, 2), max_seq_len=8192,
+                           initial_alloc_tokens=0)
+        dev = ns.VirtualMemoryDevice(ns.DeviceConfig(cfg.capacity_bytes, cfg.chunk_size_bytes))
+        sched = ns.VTensorScheduler(ns.VTensorOps(dev, ns.TensorPool(cfg.tokens_per_chunk), cfg))
+        for b in range(64):
+            sched.create(f"r{b}", [1] * 4080)
+            sched.mark_prefilled(f"r{b}")
+        ext, app = [], []
+        for k in range(1, 9):
+            for b in range(64):
+                t0 = time.perf_counter_ns()
+                sched.extend(f"r{b}", 4080 + 16 * k)  # +1 chunk
+                ext.append(time.perf_counter_ns() - t0)
+            for b in range(64):
+                for _ in range(16):
+                    t0 = time.perf_counter_ns()
+                    sched.append_token(f"r{b}", 7)
+                    app.append(time.perf_counter_ns() - t0)
+        ext.sort()
+        app.sort()
+        out[name] = {"extend_1chunk_us_p50": round(ext[len(ext) // 2] / 1e3, 2),
+                     "extend_1chunk_us_p99": round(ext[int(len(ext) * 0.99)] / 1e3, 2),
+                     "append_token_us_p50": round(app[len(app) // 2] / 1e3, 2)}
+    out["cores"] = 1
+    out["kind"] = "port"
+    return out
 
 
 def run_reference(args, world, rank):

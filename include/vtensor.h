@@ -142,6 +142,12 @@ int vt_poll(const vt_device* dev, uint64_t ticket, int* done);
 int vt_fence(vt_device* dev, void* cuda_stream);
 int vt_set_async(vt_device* dev, int enabled);
 int vt_driver_stats_get(const vt_device* dev, vt_driver_stats* out);
+/* Submit -> completed latency (ns) of every driver op of kind `op` (a vt_op
+ * code: create/map/unmap/destroy/release) completed since the last reset;
+ * copies up to `cap` samples, *n = total available. reset != 0 clears. This
+ * is the "vTensor extend latency" distribution (p50/p99) for maps. */
+int vt_driver_latencies(vt_device* dev, int32_t op, int64_t* ns_out, int64_t cap, int64_t* n,
+                        int reset);
 
 /* Device virtual address of a reserved range (CUdeviceptr), valid while the
  * range is reserved; 0 on the simulated backend. */

@@ -139,6 +139,7 @@ def vtensor_lib() -> ctypes.CDLL:
         "vt_fence": (c_int, [c_void_p, c_void_p]),
         "vt_set_async": (c_int, [c_void_p, c_int]),
         "vt_driver_stats_get": (c_int, [c_void_p, POINTER(VtDriverStats)]),
+        "vt_driver_latencies": (c_int, [c_void_p, c_int32, P64, c_int64, P64, c_int]),
         "vt_va": (c_int, [c_void_p, c_int64, POINTER(c_uint64)]),
         "vt_encode_tensor_map": (
             c_int,
@@ -161,6 +162,6 @@ VTENSOR_SYMBOLS = (
     "vt_set_active_requests", "vt_get_stats", "vt_resolve", "vt_handle_alive",
     "vt_live_handles", "vt_live_ranges", "vt_range_mappings",
     "vt_call_log_len", "vt_call_log_read", "vt_ticket", "vt_wait", "vt_poll",
-    "vt_fence", "vt_set_async", "vt_driver_stats_get", "vt_va",
+    "vt_fence", "vt_set_async", "vt_driver_stats_get", "vt_driver_latencies", "vt_va",
     "vt_encode_tensor_map",
 )

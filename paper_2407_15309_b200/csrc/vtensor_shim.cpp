@@ -194,8 +194,18 @@ struct vt_device {
   uint64_t synced_epoch = 0;                // waited by the worker
   std::unordered_map<int64_t, CUmemGenericAllocationHandle> phys;  // worker-owned
   vt_driver_stats dstats{};
+  std::mutex lat_mu;
+  std::vector<int64_t> lat[6];  // per vt_op: submit -> completed, ns
 
   bool is_cuda() const { return ordinal >= 0; }
+
+  void note_latency(const DrvOp& op, int64_t done_ns) {
+    static const int kOp[] = {VT_OP_CREATE_CHUNK, VT_OP_MAP_PAGE, VT_OP_UNMAP_PAGE,
+                              VT_OP_DESTROY_CHUNK, VT_OP_RELEASE_ADDRESS};
+    std::lock_guard<std::mutex> lk(lat_mu);
+    auto& v = lat[kOp[static_cast<int>(op.kind)]];
+    if (v.size() < (1u << 20)) v.push_back(done_ns - op.submit_ns);
+  }
   int64_t created_bytes() const {
     return static_cast<int64_t>(handles.size()) * cfg.chunk_bytes;
   }
@@ -357,7 +367,9 @@ struct vt_device {
         }
       }
     }
-    int64_t lat = now_ns() - ops[n - 1].submit_ns;
+    const int64_t done = now_ns();
+    for (size_t k = 0; k < n; ++k) note_latency(ops[k], done);
+    int64_t lat = done - ops[n - 1].submit_ns;
     dstats.max_op_ns = std::max<int64_t>(dstats.max_op_ns, lat);
     dstats.ops_completed += static_cast<int64_t>(n);
   }
@@ -816,6 +828,18 @@ int vt_set_async(vt_device* d, int enabled) {
 
 int vt_driver_stats_get(const vt_device* d, vt_driver_stats* out) {
   *out = d->dstats;
+  return VT_OK;
+}
+
+int vt_driver_latencies(vt_device* d, int32_t op, int64_t* ns_out, int64_t cap, int64_t* n,
+                        int reset) {
+  if (op < 0 || op > 5) return VT_E_ARG;
+  std::lock_guard<std::mutex> lk(d->lat_mu);
+  auto& v = d->lat[op];
+  *n = static_cast<int64_t>(v.size());
+  const int64_t k = std::min<int64_t>(cap, *n);
+  if (k > 0 && ns_out) std::memcpy(ns_out, v.data(), static_cast<size_t>(k) * sizeof(int64_t));
+  if (reset) v.clear();
   return VT_OK;
 }
 

@@ -159,7 +159,10 @@ class CallLog(Sequence):
         self._cache: list[DeviceCall] = []
 
     def __len__(self) -> int:
-        return int(self._dev._lib.vt_call_log_len(self._dev._h))
+        # every primitive appends exactly one entry per processed page and
+        # goes through the facade, so the length is tracked on the Python
+        # side (no C call on the engine's hot "calls since" arithmetic)
+        return self._dev._log_len
 
     def _fill(self, upto: int) -> None:
         have = len(self._cache)
@@ -223,6 +226,7 @@ class VirtualMemoryDevice:
         self._interned: dict[int, PhysicalHandle] = {}
         self._ranges: dict[int, VirtualRange] = {}
         self.call_log = CallLog(self)
+        self._log_len = 0
         self._i64 = ctypes.c_int64()
         self._i64b = ctypes.c_int64()
 
@@ -295,6 +299,7 @@ class VirtualMemoryDevice:
             self._raise(rc)
         rng = VirtualRange(base=base.value, length_bytes=size_bytes, page_count=pages.value)
         self._ranges[rng.base] = rng
+        self._log_len += 1
         return rng
 
     def create_chunk(self) -> PhysicalHandle:
@@ -303,6 +308,7 @@ class VirtualMemoryDevice:
             self._raise(rc)
         handle = PhysicalHandle(id=self._i64.value)
         self._interned[handle.id] = handle
+        self._log_len += 1
         return handle
 
     def map_page(self, rng: VirtualRange, page_index: int, handle: PhysicalHandle) -> None:
@@ -310,15 +316,22 @@ class VirtualMemoryDevice:
         if rc:
             self._raise(rc)
         handle.map_count += 1
+        self._log_len += 1
 
     def map_pages(self, rng: VirtualRange, first_page: int, handles: list[PhysicalHandle]) -> None:
         """Batched ``map_page`` over consecutive slots: one shim call, same log."""
         n = len(handles)
         if n == 0:
             return
-        ids = (ctypes.c_int64 * n)(*[h.id for h in handles])
-        rc = self._lib.vt_map_pages(self._h, rng.base, first_page, ids, n, ctypes.byref(self._i64))
-        done = self._i64.value
+        if n == 1:
+            rc = self._lib.vt_map_page(self._h, rng.base, first_page, handles[0].id)
+            done = 0 if rc else 1
+        else:
+            ids = (ctypes.c_int64 * n)(*[h.id for h in handles])
+            rc = self._lib.vt_map_pages(self._h, rng.base, first_page, ids, n,
+                                        ctypes.byref(self._i64))
+            done = self._i64.value
+        self._log_len += done
         for h in handles[:done]:
             h.map_count += 1
         if rc:
@@ -330,6 +343,7 @@ class VirtualMemoryDevice:
             self._raise(rc)
         handle = self._interned[self._i64.value]
         handle.map_count -= 1
+        self._log_len += 1
         return handle
 
     def unmap_tail(self, rng: VirtualRange, from_page: int, down_to: int) -> list[PhysicalHandle]:
@@ -342,6 +356,7 @@ class VirtualMemoryDevice:
                                      ctypes.byref(self._i64))
         out = []
         done = self._i64.value
+        self._log_len += done
         for i in range(done):
             h = self._interned[ids[i]]
             h.map_count -= 1
@@ -355,12 +370,14 @@ class VirtualMemoryDevice:
         if rc:
             self._raise(rc)
         self._ranges.pop(rng.base, None)
+        self._log_len += 1
 
     def destroy_chunk(self, handle: PhysicalHandle) -> None:
         rc = self._lib.vt_destroy_chunk(self._h, handle.id)
         if rc:
             self._raise(rc)
         self._interned.pop(handle.id, None)
+        self._log_len += 1
 
     # -- inspection (device.py:272-295) ---------------------------------------
 
@@ -432,6 +449,15 @@ class VirtualMemoryDevice:
 
     def set_async(self, enabled: bool) -> None:
         self._lib.vt_set_async(self._h, int(bool(enabled)))
+
+    def driver_latencies(self, op: str = "map_page", reset: bool = False) -> list[int]:
+        """Submit->completed latency (ns) of the driver ops of one kind."""
+        code = N.OP_NAMES.index(op)
+        n = ctypes.c_int64()
+        self._lib.vt_driver_latencies(self._h, code, None, 0, ctypes.byref(n), 0)
+        buf = (ctypes.c_int64 * max(n.value, 1))()
+        self._lib.vt_driver_latencies(self._h, code, buf, n.value, ctypes.byref(n), int(reset))
+        return list(buf[: n.value])
 
     def driver_stats(self) -> dict:
         s = N.VtDriverStats()
