@@ -54,6 +54,18 @@ int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
 size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t batch, int32_t max_seq_len,
                                  int32_t split_tokens);
 
+/* BASELINE, not the product path: the same CUDA-core decode kernel reading a
+ * paged KV cache (the layout the paper compares vTensor against, vLLM
+ * PagedAttention / FA_paged). Block j of request b is
+ * block_table[b*max_blocks + j] of a flat pool (block = one chunk-sized
+ * [layers][K|V][kv_heads][tpc][head_dim] tile), i.e. one dependent table
+ * lookup per block instead of VA arithmetic. */
+int vt_decode_attention_paged(const vt_kv_geometry* g, int32_t layer, const void* q,
+                              const void* pool_base, const int32_t* block_table,
+                              int32_t max_blocks, const int32_t* seq_lens, int32_t batch,
+                              int32_t max_seq_len, float scale, void* out, void* workspace,
+                              size_t workspace_bytes, int32_t split_tokens, void* stream);
+
 /* KV append (row a29): write the K/V of one new token per request at token
  * position positions[b], for layers [layer_begin, layer_begin + n_layers).
  *   k_new, v_new : [n_layers, batch, kv_heads, head_dim] bf16 */

@@ -40,6 +40,10 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_decode_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, P, c_int32, c_int32,
                                             c_float, P, P, c_size_t, c_int32, P]
         lib.vt_decode_attention.restype = c_int
+        lib.vt_decode_attention_paged.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, P,
+                                                  c_int32, c_int32, c_float, P, P, c_size_t,
+                                                  c_int32, P]
+        lib.vt_decode_attention_paged.restype = c_int
         lib.vt_decode_workspace_bytes.argtypes = [POINTER(_Geo), c_int32, c_int32, c_int32]
         lib.vt_decode_workspace_bytes.restype = c_size_t
         lib.vt_kv_append.argtypes = [POINTER(_Geo), c_int32, c_int32, P, P, P, P, c_int32, P]
@@ -55,7 +59,8 @@ def attn_lib() -> ctypes.CDLL:
     return _lib
 
 
-ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_workspace_bytes", "vt_kv_append",
+ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_paged",
+                "vt_decode_workspace_bytes", "vt_kv_append",
                 "vt_kv_tensor_maps", "vt_prefill_attention", "vt_attn_last_launches")
 
 
@@ -124,6 +129,30 @@ def decode_attention(q: torch.Tensor, kv_va: torch.Tensor, seq_lens: torch.Tenso
         max_seq_len, scale, out.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(),
         workspace.split_tokens or split_tokens, _stream(stream))
     _check(rc, "vt_decode_attention")
+    return out
+
+
+def decode_attention_paged(q: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor,
+                           seq_lens: torch.Tensor, layer: int, geo: KVGeometry, max_seq_len: int,
+                           out: torch.Tensor | None = None,
+                           workspace: DecodeWorkspace | None = None, scale: float | None = None,
+                           split_tokens: int = 0,
+                           stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """BASELINE (paper's comparison point): the CUDA-core decode over a paged
+    KV pool addressed through ``block_table`` [B, max_blocks] int32."""
+    B = q.shape[0]
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = DecodeWorkspace(geo, B, max_seq_len, split_tokens)
+    _need_cuda(q, pool, block_table, seq_lens, out)
+    if scale is None:
+        scale = 1.0 / math.sqrt(geo.head_dim)
+    rc = attn_lib().vt_decode_attention_paged(
+        ctypes.byref(_geo(geo)), layer, q.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
+        block_table.shape[1], seq_lens.data_ptr(), B, max_seq_len, scale, out.data_ptr(),
+        workspace.buf.data_ptr(), workspace.buf.numel(), split_tokens, _stream(stream))
+    _check(rc, "vt_decode_attention_paged")
     return out
 
 

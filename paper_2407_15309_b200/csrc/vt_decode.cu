@@ -62,6 +62,12 @@ struct DecodeArgs {
   int64_t k_off, v_off;   // byte offset of (layer, K|V, head 0) inside a chunk
   int64_t head_bytes;     // tpc * D * 2
   float scale_log2;
+  // Paged baseline (vt_decode_attention_paged): chunk c of request b lives at
+  // pool_base + block_table[b * max_blocks + c] * chunk_bytes instead of at
+  // kv_va[b] + c * chunk_bytes — one dependent table load per block.
+  const int32_t* block_table;
+  int32_t max_blocks;
+  uint64_t pool_base;
 };
 
 template <int G>
@@ -122,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<G>::kMinBlocks)
 
   if (warp == kConsumerWarps) {
     // ------------------------------ producer ------------------------------
-    const uint64_t va = a.kv_va[b];
+    const uint64_t va = a.block_table == nullptr ? a.kv_va[b] : 0;
     const uint64_t policy = l2_evict_first_policy();
     for (int st = 0; st < n_stage; ++st) {
       const int slot = st % kStages;
@@ -137,8 +143,13 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<G>::kMinBlocks)
         const int p0 = max(tok0, c * a.tpc);
         const int p1 = min(tok0 + ntok, (c + 1) * a.tpc);
         const uint32_t bytes = static_cast<uint32_t>(p1 - p0) * kD * 2;
-        const uint64_t src = va + static_cast<uint64_t>(c) * a.chunk_bytes +
-                             static_cast<uint64_t>(h) * a.head_bytes +
+        const uint64_t chunk_base =
+            a.block_table == nullptr
+                ? va + static_cast<uint64_t>(c) * a.chunk_bytes
+                : a.pool_base + static_cast<uint64_t>(
+                                    __ldg(&a.block_table[static_cast<int64_t>(b) * a.max_blocks + c])) *
+                                    a.chunk_bytes;
+        const uint64_t src = chunk_base + static_cast<uint64_t>(h) * a.head_bytes +
                              static_cast<uint64_t>(p0 - c * a.tpc) * kD * 2;
         const int row = p0 - tok0;
         bulk_g2s(&sm.k[slot][row * kD], src + a.k_off, bytes, &sm.full[slot], policy);
@@ -443,11 +454,12 @@ static int num_sms() {
   return n;
 }
 
-extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
-                                   const uint64_t* kv_va, const void* kv_maps,
-                                   const int32_t* seq_lens, int32_t batch, int32_t max_seq_len,
-                                   float scale, void* out, void* workspace, size_t workspace_bytes,
-                                   int32_t split_tokens, void* stream) {
+static int decode_impl(const vt_kv_geometry* g, int32_t layer, const void* q,
+                       const uint64_t* kv_va, const void* kv_maps, const int32_t* block_table,
+                       int32_t max_blocks, uint64_t pool_base, const int32_t* seq_lens,
+                       int32_t batch, int32_t max_seq_len, float scale, void* out,
+                       void* workspace, size_t workspace_bytes, int32_t split_tokens,
+                       void* stream) {
   g_last_launches = 0;
   if (g->head_dim != kD || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
   const int G = g->q_heads / g->kv_heads;
@@ -480,6 +492,9 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
   a.k_off = static_cast<int64_t>(layer * 2 + 0) * g->kv_heads * a.head_bytes;
   a.v_off = static_cast<int64_t>(layer * 2 + 1) * g->kv_heads * a.head_bytes;
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.block_table = block_table;
+  a.max_blocks = max_blocks;
+  a.pool_base = pool_base;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   dim3 grid(n_splits, g->kv_heads, batch);
   cudaError_t e;
@@ -503,4 +518,25 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
     g_last_launches = 2;
   }
   return e;
+}
+
+extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                   const uint64_t* kv_va, const void* kv_maps,
+                                   const int32_t* seq_lens, int32_t batch, int32_t max_seq_len,
+                                   float scale, void* out, void* workspace, size_t workspace_bytes,
+                                   int32_t split_tokens, void* stream) {
+  return decode_impl(g, layer, q, kv_va, kv_maps, nullptr, 0, 0, seq_lens, batch, max_seq_len,
+                     scale, out, workspace, workspace_bytes, split_tokens, stream);
+}
+
+extern "C" int vt_decode_attention_paged(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                         const void* pool_base, const int32_t* block_table,
+                                         int32_t max_blocks, const int32_t* seq_lens,
+                                         int32_t batch, int32_t max_seq_len, float scale,
+                                         void* out, void* workspace, size_t workspace_bytes,
+                                         int32_t split_tokens, void* stream) {
+  if (block_table == nullptr || pool_base == nullptr) return cudaErrorInvalidValue;
+  return decode_impl(g, layer, q, nullptr, nullptr, block_table, max_blocks,
+                     reinterpret_cast<uint64_t>(pool_base), seq_lens, batch, max_seq_len, scale,
+                     out, workspace, workspace_bytes, split_tokens, stream);
 }

@@ -108,3 +108,46 @@ def test_decode_reuses_workspace_and_is_deterministic(cuda_ok):
     torch.cuda.synchronize()
     assert torch.equal(a, b) and torch.equal(c, d)
     assert (a.float() - c.float()).abs().max() <= 2e-2 * a.float().abs().max()
+
+
+def build_paged_copy(st, kv_va, lens, seed=0):
+    """Copy every request's mapped chunks into a flat cudaMalloc'd block pool at
+    shuffled block ids (what a paged KV cache looks like) + the block table."""
+    tpc = st.cfg.tokens_per_chunk
+    nblk = [st.sched.mem[f"req{i}"].vt.space.mapped_pages for i in range(len(lens))]
+    total = sum(nblk)
+    max_blocks = max(max(nblk), 1)
+    chunk = st.cfg.chunk_size_bytes
+    pool = torch.empty(total * chunk, dtype=torch.uint8, device="cuda")
+    perm = torch.randperm(total, generator=torch.Generator().manual_seed(seed)).tolist()
+    table = torch.zeros(len(lens), max_blocks, dtype=torch.int32)
+    k = 0
+    from paper_2407_15309_b200.kv_layout import chunk_view
+
+    for b, (va, n) in enumerate(zip(kv_va.tolist(), nblk)):
+        if n == 0:
+            continue
+        src = chunk_view(va, n, st.geo).reshape(n, -1).view(torch.uint8)
+        for c in range(n):
+            blk = perm[k]
+            k += 1
+            pool[blk * chunk:(blk + 1) * chunk].copy_(src[c])
+            table[b, c] = blk
+    return pool, table.cuda()
+
+
+@pytest.mark.gpu
+def test_paged_baseline_matches_vtensor(cuda_ok):
+    """The paged baseline reads the same KV through a block table and must give
+    bit-identical results to the vTensor CUDA-core path (same kernel)."""
+    from paper_2407_15309_b200.attention import decode_attention_paged
+
+    st = cuda_stack(32, 8, 32, 4352)
+    lens = [1, 15, 16, 17, 300, 2049, 4096]
+    kv_va, seq = admit_with_lengths(st, lens, seed=21)
+    pool, table = build_paged_copy(st, kv_va, lens)
+    q = torch.randn(len(lens), 32, 128, device="cuda").to(torch.bfloat16)
+    a = decode_attention(q, kv_va, seq, 9, st.geo, max(lens), split_tokens=512)
+    b = decode_attention_paged(q, pool, table, seq, 9, st.geo, max(lens), split_tokens=512)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

@@ -1,0 +1,73 @@
+"""Restate the paper's kernel comparison on B200:
+vTensor decode (no block table) vs a paged-KV decode (block table, same data)
+on config 2. 32 back-to-back layer launches each; same bytes, same kernel
+family. Prints one JSON line."""
+
+import json
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+
+import torch  # noqa: E402
+
+from paper_2407_15309_b200.attention import (DecodeWorkspace, decode_attention,  # noqa: E402
+                                             decode_attention_paged, kv_tensor_maps)
+from test_decode_gpu import build_paged_copy  # noqa: E402
+from vt_gpu_util import admit_with_lengths, cuda_stack  # noqa: E402
+
+
+def timed32(fn, L=32, reps=3):
+    for i in range(3):
+        fn(i % L)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for layer in range(L):
+            fn(layer)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / L)
+    return best * 1e3
+
+
+def main():
+    torch.cuda.set_device(0)
+    B, ctx = 64, 4096
+    st = cuda_stack(32, 8, 32, ctx + 256, capacity_chunks=20000)
+    kv_va, seq = admit_with_lengths(st, [ctx] * B, seed=5)
+    pool, table = build_paged_copy(st, kv_va, [ctx] * B)
+    q = torch.randn(B, 32, 128, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    tpc = st.cfg.tokens_per_chunk
+    maps = kv_tensor_maps(kv_va.tolist(), [st.sched.mem[f"req{i}"].vt.space.mapped_pages * tpc
+                                           for i in range(B)], st.geo)
+    nbytes = 2 * B * ctx * 8 * 128 * 2 + 2 * B * 32 * 128 * 2
+    res = {}
+    for split in (512, 1024):
+        ws = DecodeWorkspace(st.geo, B, ctx, split)
+        res[f"paged_cuda_core_split{split}"] = timed32(
+            lambda l: decode_attention_paged(q, pool, table, seq, l, st.geo, ctx, out=out,
+                                             workspace=ws, split_tokens=split))
+        res[f"vtensor_cuda_core_split{split}"] = timed32(
+            lambda l: decode_attention(q, kv_va, seq, l, st.geo, ctx, out=out, workspace=ws,
+                                       split_tokens=split))
+    ws = DecodeWorkspace(st.geo, B, ctx)
+    res["vtensor_tcgen05_auto"] = timed32(
+        lambda l: decode_attention(q, kv_va, seq, l, st.geo, ctx, out=out, workspace=ws,
+                                   kv_maps=maps))
+    gbs = {k: round(nbytes / (v * 1e-6) / 1e9, 1) for k, v in res.items()}
+    best_paged = min(v for k, v in res.items() if k.startswith("paged"))
+    print(json.dumps({"config": "cfg2 B64 ctx4096 32q/8kv, 32 back-to-back layers",
+                      "us_per_layer": {k: round(v, 2) for k, v in res.items()}, "GB/s": gbs,
+                      "speedup_vtensor_tc_over_best_paged": round(best_paged / res["vtensor_tcgen05_auto"], 3),
+                      "speedup_vtensor_cc_over_paged_same_kernel": round(
+                          res["paged_cuda_core_split1024"] / res["vtensor_cuda_core_split1024"], 3)}))
+
+
+if __name__ == "__main__":
+    main()
