@@ -1,28 +1,44 @@
 // Prefill / prefix-prefill attention over a vTensor KV cache — tcgen05 + TMEM +
 // TMA, sm_100a (row a28).
 //
-// CTA = (request b, q head h, tile of 128 new query tokens). The new tokens sit
-// at absolute positions [start_b, start_b + n_new) and attend causally to the
-// cache [0, pos]; the first start_b keys are the rTree-shared prefix chunks,
-// which are mapped into the request's own VA (hard links), so the kernel reads
-// them in place through the same TMA descriptor — no gather, no block table.
+// CTA = (request b, q-head pair {h0, h0+1} of one GQA group, tile of 128 new
+// query tokens). The new tokens sit at absolute positions
+// [start_b, start_b + n_new) and attend causally to the cache [0, pos]; the
+// first start_b keys are the rTree-shared prefix chunks, mapped into the
+// request's own VA (hard links), so the kernel reads them in place through the
+// request's TMA descriptor — no gather, no block table.
 //
-// Warp roles (192 threads):
-//   warp 0    TMA producer: Q tile once; K and V tiles of 128 keys into a
-//             2-stage ring (cp.async.bulk.tensor, SWIZZLE_128B). K/V come from
-//             a per-request 4-D tensor map over the request VA
-//             (d, token-in-chunk, (layer,K|V,head) block, chunk) whose chunk
-//             extent is ceil(kv_len/tpc): the TMA never touches unmapped VA.
-//   warp 1    MMA issuer (one thread): S_j = Q K_j^T into a double-buffered
-//             TMEM tile (tcgen05.mma kind::f16, M=128 N=128, K-major A and B),
-//             then O += P_j V_j (A = P from smem K-major, B = V MN-major) into a
-//             TMEM accumulator. S_{j+1} is issued before PV_j so the tensor
-//             core works while softmax_j runs. Completion via tcgen05.commit.
-//   warps 2-5 softmax / correction / epilogue, thread <-> TMEM lane <-> query
-//             row: tcgen05.ld of S, causal + length mask, online softmax in
-//             the exp2 domain, O rescale in TMEM (tcgen05.ld/st, skipped when
-//             no row of the warp moved its max), P -> smem as bf16 in the
-//             SW128 K-major layout, final O / l -> bf16 -> global.
+// The two heads of a pair ("slots") share every K/V tile and have identical
+// masks, so one TMA stream feeds two independent softmax pipelines. Scores are
+// computed in 64-key blocks into a per-slot double buffer, so the tensor core
+// computes S(i+1) of both slots while the softmax warpgroups turn S(i) into
+// P(i); the PV MMAs follow. (For odd GQA groups, e.g. MHA, a CTA runs one
+// slot.)
+//
+// Warp roles (384 threads; registers moved to the softmax warpgroups with
+// setmaxnreg):
+//   warp 8     TMA producer: both slots' Q tiles once; K and V tiles of 128
+//              keys into 2-stage rings (cp.async.bulk.tensor, SWIZZLE_128B).
+//              K/V come from a per-request 4-D tensor map over the request VA
+//              (d, token-in-chunk, (layer,K|V,head) block, chunk) whose chunk
+//              extent is ceil(kv_len/tpc): the TMA never touches unmapped VA.
+//   warp 9     MMA issuer (one thread), per 64-key block i and slot s:
+//                S_s(i)   = Q_s K_i^T   (SS: both operands in smem) -> TMEM
+//                O_s     += P_s(i) V_i  (TS: P read from TMEM, V MN-major smem)
+//              issued as S(i+1), PV(i): S(i+1) overwrites the buffer of P(i-1)
+//              only after the PV that consumed it (tcgen05.mma executes in
+//              issue order).
+//   warps 0-3  softmax slot 0;  warps 4-7  softmax slot 1. Thread <-> TMEM
+//              lane <-> query row: tcgen05.ld of S, causal + length mask, online
+//              softmax in the exp2 domain with a lazy running max (O and l are
+//              rescaled only when a row's max grows by more than 2^8, which is
+//              exact because numerator and denominator share the stale max),
+//              packed fp32x2 arithmetic, a quarter of the exponentials on the
+//              FMA pipe (polynomial) to offload MUFU, P -> TMEM as packed bf16
+//              over its S buffer, final O / l -> bf16 -> global.
+//
+// TMEM (512 columns): slot s has score buffers at 128 s + {0, 64} (64 columns
+// each; P(i) takes the first 32) and O at [256 + 128 s, 384 + 128 s).
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -36,59 +52,40 @@ namespace vt {
 namespace pf {
 
 constexpr int BM = 128;
-constexpr int BN = 128;
+constexpr int BN = 128;  // keys per K/V tile (TMA)
+constexpr int BS = 64;   // keys per score block (S double-buffered per slot)
 constexpr int D = 128;
 constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kSlots = 2;
+constexpr int kThreads = kSlots * 128 + 128;  // softmax WGs, then TMA/MMA WG
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kOCol = 256;  // S double buffer at columns 0 and 128
+constexpr uint32_t kOCol = 256;
+constexpr float kRescaleLog2 = 8.0f;  // lazy max: rescale only when it grows by > 2^8
+#ifndef VT_PF_POLY_LANE
+#define VT_PF_POLY_LANE 3
+#endif
+constexpr int kPolyLane = VT_PF_POLY_LANE;  // pair k with k % 4 == this: exp2 on the FMA pipe
 
 struct __align__(1024) Smem {
-  __nv_bfloat16 q[2][BM * 64];            // SW128 K-major: d 0-63 | d 64-127
+  __nv_bfloat16 q[kSlots][2][BM * 64];    // SW128 K-major: d 0-63 | d 64-127
   __nv_bfloat16 k[kStages][2][BN * 64];   // SW128 K-major (keys x d)
   __nv_bfloat16 v[kStages][2][BN * 64];   // SW128, read as MN-major B (d x keys)
-  __nv_bfloat16 p[2][BM * 64];            // SW128 K-major: keys 0-63 | 64-127
   uint64_t q_full;
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2];
-  uint64_t p_full;
-  uint64_t pv_done;
+  uint64_t s_full[kSlots][2];
+  uint64_t p_full[kSlots][2];
+  uint64_t o_done[kSlots];
   uint32_t tmem_base;
 };
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
-__device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo_bytes, uint32_t sbo_bytes) {
-  const uint64_t a = smem_u32(p);
-  return ((a >> 4) & 0x3FFFull) | (static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16) |
-         (static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
-}
-
-// Instruction descriptor: bf16 x bf16 -> f32, M=128, N=128, A K-major.
-__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
-         (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id,
-                                     uint32_t acc) {
+// D[tmem] (+)= A[tmem] * B[smem desc]   (A = P, 128 lanes x 16 bf16 keys)
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id,
+                                       uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(id), "r"(acc));
 }
 
 #define VT_R32(x)                                                                              \
@@ -104,15 +101,15 @@ __device__ __forceinline__ void tc_fence_after() {
       "r"(x[22]), "r"(x[23]), "r"(x[24]), "r"(x[25]), "r"(x[26]), "r"(x[27]), "r"(x[28]),      \
       "r"(x[29]), "r"(x[30]), "r"(x[31])
 
-// 32 consecutive fp32 columns of this thread's TMEM lane.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// 32 consecutive 32-bit TMEM columns of this thread's lane (no wait).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
       "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : VT_R32(r)
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
       "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
@@ -120,29 +117,37 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       VT_W32(r)
       : "memory");
 }
-__device__ __forceinline__ void tmem_wait_ld() {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() {
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 2^x for a pair on the FMA pipe (offloads MUFU): round-to-nearest split
+// x = n + f, f in [-1/2, 1/2], cubic fit of 2^f (max relative error 1.1e-4,
+// far below the 3.9e-3 of the bf16 P it feeds), exponent added as integer
+// bits. Clamped at -125 (2^-125 ~ 2e-38 stands in for exp(-inf) = 0: P of a
+// masked key is that small, and masked V rows are finite or zeroed); x <= 127.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 big = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, big);                       // n in the low mantissa bits
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
+  float2 p = __ffma2_rn(make_float2(0.054598168f, 0.054598168f), f,
+                        make_float2(0.24221788f, 0.24221788f));
+  p = __ffma2_rn(p, f, make_float2(0.69336749f, 0.69336749f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 struct Args {
   __nv_bfloat16* out;       // [B, n_new, Hq, D]
   const CUtensorMap* kv;    // [B] per-request maps
   const int32_t* start;     // [B]
-  int32_t n_new, hq, hkv, tpc, layer;
+  int32_t n_new, hq, hkv, tpc, layer, slots;
   float scale_log2;
 };
 
@@ -153,20 +158,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       ~static_cast<uintptr_t>(1023));
   const int n_qtiles = gridDim.x;
   const int t = n_qtiles - 1 - static_cast<int>(blockIdx.x);  // longest tiles first
-  const int h = blockIdx.y;
+  const int nslots = a.slots;
+  const int h0 = blockIdx.y * nslots;
   const int b = blockIdx.z;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int start = a.start[b];
   const int kv_len = start + a.n_new;
   const int q_last = min(a.n_new, (t + 1) * BM);  // exclusive, relative to start
-  const int n_kv = (start + q_last + BN - 1) / BN;
-  const int hk = h / (a.hq / a.hkv);
+  const int n_sub = (start + q_last + BS - 1) / BS;  // 64-key score blocks
+  const int n_kv = (n_sub + 1) / 2;                  // 128-key K/V tiles
+  const int hk = h0 / (a.hq / a.hkv);
   const int blk_k = (a.layer * 2 + 0) * a.hkv + hk;
   const int blk_v = (a.layer * 2 + 1) * a.hkv + hk;
   const CUtensorMap* kvmap = a.kv + b;
+  constexpr int kTmaWarp = kSlots * 4, kMmaWarp = kSlots * 4 + 1;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     mbar_init(&sm.q_full, 1);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.k_full[i], 1);
@@ -174,218 +182,275 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.v_full[i], 1);
       mbar_init(&sm.v_empty[i], 1);
     }
-    mbar_init(&sm.s_full[0], 1);
-    mbar_init(&sm.s_full[1], 1);
-    mbar_init(&sm.p_full, 128);
-    mbar_init(&sm.pv_done, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      for (int u = 0; u < 2; ++u) {
+        mbar_init(&sm.s_full[s][u], 1);
+        mbar_init(&sm.p_full[s][u], 128);
+      }
+      mbar_init(&sm.o_done[s], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
+  if (warp == kMmaWarp) tc::alloc(&sm.tmem_base, kTmemCols);
+  tc::fence_before();
   __syncthreads();
-  tc_fence_after();
+  tc::fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------ TMA producer ------------------------------
-    if (lane == 0) {
-      tma_prefetch_desc(&q_map);
-      tma_prefetch_desc(kvmap);
-      const uint64_t keep = l2_evict_last_policy();   // K/V re-read by the group's heads
-      const uint64_t once = l2_evict_first_policy();
-      mbar_arrive_expect_tx(&sm.q_full, 2 * BM * 64 * 2);
-      tma_load_4d(sm.q[0], &q_map, &sm.q_full, 0, h, t * BM, b, once);
-      tma_load_4d(sm.q[1], &q_map, &sm.q_full, 64, h, t * BM, b, once);
-      for (int j = 0; j < n_kv; ++j) {
-        const int s = j % kStages;
-        const uint32_t ph = (j / kStages) & 1;
-        const int tok0 = j * BN;
-        const int c1 = tok0 % a.tpc;
-        const int c3 = tok0 / a.tpc;
-        if (j >= kStages) mbar_wait(&sm.k_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&sm.k_full[s], 2 * BN * 64 * 2);
-        tma_load_4d(sm.k[s][0], kvmap, &sm.k_full[s], 0, c1, blk_k, c3, keep);
-        tma_load_4d(sm.k[s][1], kvmap, &sm.k_full[s], 64, c1, blk_k, c3, keep);
-        if (j >= kStages) mbar_wait(&sm.v_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&sm.v_full[s], 2 * BN * 64 * 2);
-        tma_load_4d(sm.v[s][0], kvmap, &sm.v_full[s], 0, c1, blk_v, c3, keep);
-        tma_load_4d(sm.v[s][1], kvmap, &sm.v_full[s], 64, c1, blk_v, c3, keep);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ------------------------------- MMA issuer -------------------------------
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc(false);
-      constexpr uint32_t id_pv = idesc(true);
-      mbar_wait(&sm.q_full, 0);
-      auto issue_pv = [&](int i) {
-        mbar_wait(&sm.p_full, i & 1);
-        mbar_wait(&sm.v_full[i % kStages], (i / kStages) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t ad = sdesc(reinterpret_cast<const uint8_t*>(sm.p[kk >> 2]) + 32 * (kk & 3),
-                                    16, 1024);
-          const uint64_t bd = sdesc(reinterpret_cast<const uint8_t*>(sm.v[i % kStages][0]) +
-                                        kk * 16 * 128,
-                                    BN * 128, 1024);
-          umma(tmem + kOCol, ad, bd, id_pv, (i > 0 || kk > 0) ? 1u : 0u);
+  if (warp >= kSlots * 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    if (warp == kTmaWarp) {
+      // ------------------------------ TMA producer ------------------------------
+      if (lane == 0) {
+        tma_prefetch_desc(&q_map);
+        tma_prefetch_desc(kvmap);
+        const uint64_t keep = l2_evict_last_policy();   // K/V re-read by the group's heads
+        const uint64_t once = l2_evict_first_policy();
+        mbar_arrive_expect_tx(&sm.q_full, nslots * 2 * BM * 64 * 2);
+        for (int s = 0; s < nslots; ++s) {
+          tma_load_4d(sm.q[s][0], &q_map, &sm.q_full, 0, h0 + s, t * BM, b, once);
+          tma_load_4d(sm.q[s][1], &q_map, &sm.q_full, 64, h0 + s, t * BM, b, once);
         }
-        umma_commit(&sm.pv_done);
-        umma_commit(&sm.v_empty[i % kStages]);
+        for (int j = 0; j < n_kv; ++j) {
+          const int st = j % kStages;
+          const uint32_t ph = (j / kStages) & 1;
+          const int tok0 = j * BN;
+          const int c1 = tok0 % a.tpc;
+          const int c3 = tok0 / a.tpc;
+          if (j >= kStages) mbar_wait(&sm.k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&sm.k_full[st], 2 * BN * 64 * 2);
+          tma_load_4d(sm.k[st][0], kvmap, &sm.k_full[st], 0, c1, blk_k, c3, keep);
+          tma_load_4d(sm.k[st][1], kvmap, &sm.k_full[st], 64, c1, blk_k, c3, keep);
+          if (j >= kStages) mbar_wait(&sm.v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&sm.v_full[st], 2 * BN * 64 * 2);
+          tma_load_4d(sm.v[st][0], kvmap, &sm.v_full[st], 0, c1, blk_v, c3, keep);
+          tma_load_4d(sm.v[st][1], kvmap, &sm.v_full[st], 64, c1, blk_v, c3, keep);
+        }
+      }
+      __syncwarp();
+    } else if (warp == kMmaWarp) {
+      // ------------------------------- MMA issuer -------------------------------
+      // Order: S(0); then per score block i: S(i+1) for every slot, PV(i) for
+      // every slot. S(i+1) lands in the TMEM buffer that held P(i-1), whose PV
+      // was issued one step earlier (tcgen05.mma runs in issue order). The
+      // whole warp walks the schedule so descriptors stay warp-uniform (uniform
+      // registers); one elected lane issues each MMA group and its commits.
+      constexpr uint32_t id_s = tc::idesc_bf16(BM, BS, false, false);
+      constexpr uint32_t id_pv = tc::idesc_bf16(BM, D, false, true);
+      // Descriptor address fields count 16 B units: a [.][64] bf16 tile half
+      // is 16 KiB = 1024 units, 64 keys = 512, one 16-element K step inside a
+      // SW128 row = 2, 16 keys of V = 128.
+      const uint64_t dq = tc::sdesc(sm.q[0][0], 16, 1024);
+      const uint64_t dk = tc::sdesc(sm.k[0][0], 16, 1024);
+      const uint64_t dv = tc::sdesc(sm.v[0][0], BN * 128, 1024);
+      auto issue_s = [&](int s, int i) {
+        const int st = (i >> 1) % kStages;
+        const uint32_t d = tmem + static_cast<uint32_t>(s * 2 * BS + (i & 1) * BS);
+        const uint64_t a0 = dq + static_cast<uint64_t>(s * 2048);
+        const uint64_t b0 = dk + static_cast<uint64_t>(st * 2048 + (i & 1) * 512);
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off = static_cast<uint64_t>((kk >> 2) * 1024 + 2 * (kk & 3));
+            tc::mma(d, a0 + off, b0 + off, id_s, kk > 0 ? 1u : 0u);
+          }
+          tc::commit(&sm.s_full[s][i & 1]);
+        }
+        __syncwarp();
       };
-      for (int j = 0; j < n_kv; ++j) {
-        const int s = j % kStages;
-        mbar_wait(&sm.k_full[s], (j / kStages) & 1);
-        tc_fence_after();
-        const uint32_t sc = static_cast<uint32_t>((j & 1) * BN);
+      auto issue_pv = [&](int s, int i) {
+        const int st = (i >> 1) % kStages;
+        mbar_wait(&sm.p_full[s][i & 1], (i >> 1) & 1);
+        tc::fence_after();
+        const uint32_t d = tmem + kOCol + static_cast<uint32_t>(s * D);
+        const uint32_t p = tmem + static_cast<uint32_t>(s * 2 * BS + (i & 1) * BS);
+        const uint64_t b0 = dv + static_cast<uint64_t>(st * 2048 + (i & 1) * 512);
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t ad = sdesc(reinterpret_cast<const uint8_t*>(sm.q[kk >> 2]) + 32 * (kk & 3),
-                                    16, 1024);
-          const uint64_t bd = sdesc(reinterpret_cast<const uint8_t*>(sm.k[s][kk >> 2]) + 32 * (kk & 3),
-                                    16, 1024);
-          umma(tmem + sc, ad, bd, id_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < BS / 16; ++kk)
+            mma_ts(d, p + 8 * kk, b0 + static_cast<uint64_t>(kk * 128), id_pv,
+                   (i > 0 || kk > 0) ? 1u : 0u);
+          tc::commit(&sm.o_done[s]);
         }
-        umma_commit(&sm.s_full[j & 1]);
-        umma_commit(&sm.k_empty[s]);
-        if (j >= 1) issue_pv(j - 1);
+        __syncwarp();
+      };
+      auto commit1 = [&](uint64_t* bar) {
+        if (tc::elect_one()) tc::commit(bar);
+        __syncwarp();
+      };
+      mbar_wait(&sm.q_full, 0);
+      mbar_wait(&sm.k_full[0], 0);
+      tc::fence_after();
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s)
+        if (s < nslots) issue_s(s, 0);
+      if (n_sub == 1) commit1(&sm.k_empty[0]);
+      for (int i = 0; i < n_sub; ++i) {
+        const int nx = i + 1;
+        if (nx < n_sub) {
+          const int tile = nx >> 1;
+          if ((nx & 1) == 0) {
+            mbar_wait(&sm.k_full[tile % kStages], (tile / kStages) & 1);
+            tc::fence_after();
+          }
+#pragma unroll
+          for (int s = 0; s < kSlots; ++s)
+            if (s < nslots) issue_s(s, nx);
+          if ((nx & 1) == 1 || nx == n_sub - 1) commit1(&sm.k_empty[tile % kStages]);
+        }
+        const int tile = i >> 1;
+        if ((i & 1) == 0) mbar_wait(&sm.v_full[tile % kStages], (tile / kStages) & 1);
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s)
+          if (s < nslots) issue_pv(s, i);
+        if ((i & 1) == 1 || i == n_sub - 1) commit1(&sm.v_empty[tile % kStages]);
       }
-      issue_pv(n_kv - 1);
+      __syncwarp();
     }
-    __syncwarp();
   } else {
-    // ------------------------ softmax / correction / out ----------------------
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const int qpos = start + t * BM + row;  // absolute position of this query row
-    float m_run = -INFINITY, l_run = 0.f;
-    const float sl2 = a.scale_log2;
-    for (int j = 0; j < n_kv; ++j) {
-      const int kpos0 = j * BN;
-      mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      float s[BN];
-      {
-        uint32_t r[32];
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    if (warp / 4 < nslots) {
+      // ------------------------------ softmax slot s ------------------------------
+      const int s = warp / 4;
+      const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+      const int row = quarter * 32 + lane;
+      const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+      const uint32_t s_addr = lane_addr + static_cast<uint32_t>(s * 2 * BS);
+      const uint32_t o_addr = lane_addr + kOCol + static_cast<uint32_t>(s * D);
+      const int qpos = start + t * BM + row;  // absolute position of this query row
+      const int qmin = start + t * BM;        // smallest query position of the tile
+      float m_run = -INFINITY, l_run = 0.f;
+      const float sl2 = a.scale_log2;
+      for (int i = 0; i < n_sub; ++i) {
+        const int kpos0 = i * BS;
+        const uint32_t sb = s_addr + static_cast<uint32_t>((i & 1) * BS);
+        mbar_wait(&sm.s_full[s][i & 1], (i >> 1) & 1);
+        tc::fence_after();
+        float x[BS];
+        {
+          uint32_t r[BS];
+          tmem_ld32(sb, r);
+          tmem_ld32(sb + 32, r + 32);
+          tc::wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          tmem_ld32(lane_addr + (j & 1) * BN + 32 * c, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[32 * c + i] = __uint_as_float(r[i]);
+          for (int k = 0; k < BS; ++k) x[k] = __uint_as_float(r[k]);
         }
-      }
-      const bool edge = kpos0 + BN - 1 > start + t * BM || kpos0 + BN > kv_len;
-      if (edge) {
+        if (kpos0 + BS - 1 > qmin || kpos0 + BS > kv_len) {
+          const int lim = min(qpos + 1, kv_len) - kpos0;  // keys [0, lim) are visible
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
-          const int kp = kpos0 + i;
-          if (kp > qpos || kp >= kv_len) s[i] = -INFINITY;
+          for (int k = 0; k < BS; ++k)
+            if (k >= lim) x[k] = -INFINITY;
         }
-      }
-      float mx = s[0];
+        float mx;
+        {
+          float m8[8];
 #pragma unroll
-      for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
-      const float m_new = fmaxf(m_run, mx * sl2);
-      const float alpha = ex2(m_run - m_new);
-      float sum = 0.f;
+          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(x[k], x[k + 8]);
 #pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        s[i] = ex2(fmaf(s[i], sl2, -m_new));
-        sum += s[i];
-      }
-      l_run = l_run * alpha + sum;
-      m_run = m_new;
-
-      if (j >= 1) {
-        mbar_wait(&sm.pv_done, (j - 1) & 1);  // PV_{j-1} done: P free, O stable
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          for (int k = 16; k < BS; k += 16)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(x[k + u], x[k + 8 + u]));
+          mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                     fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        }
+        const float mx_s = mx * sl2;
+        const bool grow = mx_s > m_run + kRescaleLog2;  // false while both are -inf
+        const float m_new = grow ? mx_s : m_run;
+        const float alpha = grow ? tc::ex2(m_run - m_new) : 1.f;
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        const float2 sl2v = make_float2(sl2, sl2);
+        const float2 negm = make_float2(-m_use, -m_use);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        uint32_t pr[BS / 2];
+#pragma unroll
+        for (int k = 0; k < BS / 2; ++k) {
+          float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
+          if ((k & 3) == kPolyLane) {
+            e = ex2_poly2(e);
+          } else {
+            e.x = tc::ex2(e.x);
+            e.y = tc::ex2(e.y);
+          }
+          acc[k & 3] = __fadd2_rn(acc[k & 3], e);
+          pr[k] = pack_bf16(e.x, e.y);
+        }
+        const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+        l_run = fmaf(l_run, alpha, a01.x + a01.y);
+        m_run = m_new;
+        // P -> TMEM over the score buffer: column c = keys (2c, 2c+1) as bf16x2.
+        tmem_st32(sb, pr);
+        if (i >= 1 && __any_sync(0xffffffffu, grow)) {
+          mbar_wait(&sm.o_done[s], (i - 1) & 1);  // PV(i-1) done: O stable
+          tc::fence_after();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t r[32];
-            tmem_ld32(lane_addr + kOCol + 32 * c, r);
-            tmem_wait_ld();
+            tmem_ld32(o_addr + 32 * c, r);
+            tc::wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(lane_addr + kOCol + 32 * c, r);
-          }
-          tmem_wait_st();
-        }
-      }
-      if (j == n_kv - 1 && kpos0 + BN > kv_len) {
-        // Rows past kv_len may hold stale/uninitialised bytes of the last
-        // mapped chunk: zero them so 0 * NaN cannot reach the accumulator.
-        const int s = j % kStages;
-        mbar_wait(&sm.v_full[s], (j / kStages) & 1);
-        if (kpos0 + row >= kv_len) {
-          uint4 z = make_uint4(0, 0, 0, 0);
-          uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[s][0]) + row * 128);
-          uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[s][1]) + row * 128);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            r0[c] = z;
-            r1[c] = z;
+            for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
+            tmem_st32(o_addr + 32 * c, r);
           }
         }
-      }
-      // P row -> smem, bf16, SW128 K-major: 16-byte chunk c of the 128-byte
-      // row r lives at position c ^ (r % 8).
+        bool zeroed = false;
+        if (s == 0 && i == n_sub - 1 && (i | 1) * BS + BS > kv_len) {
+          // Rows past kv_len may hold stale/uninitialised bytes of the last
+          // mapped chunk: zero them so 0 * NaN cannot reach the accumulator.
+          // (Earlier PVs read only rows below kv_len; slot 1's PV of this block
+          // is issued after slot 0's P arrives.)
+          const int tile = i >> 1;
+          const int st = tile % kStages;
+          mbar_wait(&sm.v_full[st], (tile / kStages) & 1);
+          if (tile * BN + row >= kv_len) {
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][0]) + row * 128);
+            uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][1]) + row * 128);
 #pragma unroll
-      for (int ci = 0; ci < BN / 8; ++ci) {
-        const int kb = ci >> 3;
-        const int c = ci & 7;
-        uint4 w;
-        w.x = pack_bf16(s[8 * ci + 0], s[8 * ci + 1]);
-        w.y = pack_bf16(s[8 * ci + 2], s[8 * ci + 3]);
-        w.z = pack_bf16(s[8 * ci + 4], s[8 * ci + 5]);
-        w.w = pack_bf16(s[8 * ci + 6], s[8 * ci + 7]);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.p[kb]) + row * 128 +
-                                  ((c ^ (row & 7)) << 4)) = w;
+            for (int c = 0; c < 8; ++c) {
+              r0[c] = z;
+              r1[c] = z;
+            }
+          }
+          zeroed = true;
+        }
+        tc::wait_st();
+        if (zeroed) fence_proxy_async_smem();
+        tc::fence_before();
+        mbar_arrive(&sm.p_full[s][i & 1]);
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&sm.p_full);
-    }
-    // epilogue
-    mbar_wait(&sm.pv_done, (n_kv - 1) & 1);
-    tc_fence_after();
-    const int tok = t * BM + row;
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    __nv_bfloat16* dst = a.out + ((static_cast<int64_t>(b) * a.n_new + tok) * a.hq + h) * D;
+      // epilogue. o_done completes once per PV. S(n_sub-1) completing only
+      // proves PV(n_sub-3) done (S(i+1) is issued ahead of PV(i)), so step
+      // through the last two phases in order: a parity wait is only
+      // unambiguous one phase ahead.
+      if (n_sub >= 2) mbar_wait(&sm.o_done[s], (n_sub - 2) & 1);
+      mbar_wait(&sm.o_done[s], (n_sub - 1) & 1);
+      tc::fence_after();
+      const int tok = t * BM + row;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      __nv_bfloat16* dst =
+          a.out + ((static_cast<int64_t>(b) * a.n_new + tok) * a.hq + (h0 + s)) * D;
+      uint32_t r[D];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
-      tmem_ld32(lane_addr + kOCol + 32 * c, r);
-      tmem_wait_ld();
+      for (int c = 0; c < 4; ++c) tmem_ld32(o_addr + 32 * c, r + 32 * c);
+      tc::wait_ld();
       if (tok < a.n_new) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
+        for (int k = 0; k < D; k += 8) {
           uint4 w;
-          w.x = pack_bf16(__uint_as_float(r[i + 0]) * inv, __uint_as_float(r[i + 1]) * inv);
-          w.y = pack_bf16(__uint_as_float(r[i + 2]) * inv, __uint_as_float(r[i + 3]) * inv);
-          w.z = pack_bf16(__uint_as_float(r[i + 4]) * inv, __uint_as_float(r[i + 5]) * inv);
-          w.w = pack_bf16(__uint_as_float(r[i + 6]) * inv, __uint_as_float(r[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + 32 * c + i) = w;
+          w.x = pack_bf16(__uint_as_float(r[k + 0]) * inv, __uint_as_float(r[k + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(r[k + 2]) * inv, __uint_as_float(r[k + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(r[k + 4]) * inv, __uint_as_float(r[k + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(r[k + 6]) * inv, __uint_as_float(r[k + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + k) = w;
         }
       }
     }
   }
-  tc_fence_before();
+  tc::fence_before();
   __syncthreads();
-  tc_fence_after();
-  if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
-  }
+  tc::fence_after();
+  if (warp == kMmaWarp) tc::dealloc(tmem, kTmemCols);
 }
 
 }  // namespace pf
@@ -407,6 +472,7 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   const cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(BM), 1};
   int rc = vt::encode_tensor_map_bf16(&qmap, const_cast<void*>(q), 4, dims, strides, box);
   if (rc) return rc;
+  const int group = g->q_heads / g->kv_heads;
   Args a{};
   a.out = static_cast<__nv_bfloat16*>(out);
   a.kv = static_cast<const CUtensorMap*>(kv_maps);
@@ -416,6 +482,10 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   a.hkv = g->kv_heads;
   a.tpc = g->tokens_per_chunk;
   a.layer = layer;
+  a.slots = group % kSlots == 0 ? kSlots : 1;
+#ifdef VT_PF_SLOTS1
+  a.slots = 1;
+#endif  // a pair never straddles two kv heads
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t smem = sizeof(Smem) + 1024;
   static bool attr = false;
@@ -424,7 +494,7 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
                          static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid((n_new + BM - 1) / BM, g->q_heads, batch);
+  dim3 grid((n_new + BM - 1) / BM, g->q_heads / a.slots, batch);
   prefill_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(qmap, a);
   return cudaGetLastError();
 }

@@ -40,6 +40,16 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
                : "memory");
 }
 
+// One lane of a converged warp (elect.sync): warp-uniform operands stay in
+// uniform registers, and only the elected lane issues the tcgen05 op.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+C=paper_2407_15309_b200/csrc
+for V in "$@"; do
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -shared $V -o paper_2407_15309_b200/libvtattn.so $C/vt_decode.cu $C/vt_decode_tc.cu $C/vt_kvops.cu $C/vt_prefill.cu $C/vt_tmap.cu
+  echo "=== variant $V"; python tools/debug_prefill.py 2>&1 | grep -E "case|bad"
+done
