@@ -482,10 +482,7 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   a.hkv = g->kv_heads;
   a.tpc = g->tokens_per_chunk;
   a.layer = layer;
-  a.slots = group % kSlots == 0 ? kSlots : 1;
-#ifdef VT_PF_SLOTS1
-  a.slots = 1;
-#endif  // a pair never straddles two kv heads
+  a.slots = group % kSlots == 0 ? kSlots : 1;  // a pair never straddles two kv heads
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t smem = sizeof(Smem) + 1024;
   static bool attr = false;
