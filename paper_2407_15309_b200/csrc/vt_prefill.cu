@@ -9,11 +9,13 @@
 // request's TMA descriptor — no gather, no block table.
 //
 // The two heads of a pair ("slots") share every K/V tile and have identical
-// masks, so one TMA stream feeds two independent softmax pipelines. Scores are
-// computed in 64-key blocks into a per-slot double buffer, so the tensor core
-// computes S(i+1) of both slots while the softmax warpgroups turn S(i) into
-// P(i); the PV MMAs follow. (For odd GQA groups, e.g. MHA, a CTA runs one
-// slot.)
+// masks, so one TMA stream feeds two independent softmax pipelines and the
+// tensor core alternates between them: while softmax warpgroup 0 turns S0(j)
+// into P0(j), the tensor core runs slot 1's {PV1(j-1), S1(j)} and vice versa.
+// (For odd GQA groups, e.g. MHA, a CTA runs one slot.) Every MMA is
+// M128 x N128 x K16: on sm_100a switching between N=64 and N=128 shapes drains
+// the tensor pipe (tools/mma_probe.cu: an 8 x N64 + 4 x N128 mix runs at 53% of
+// the rate of either shape alone), so scores are computed in 128-key blocks.
 //
 // Warp roles (384 threads; registers moved to the softmax warpgroups with
 // setmaxnreg):
@@ -22,12 +24,13 @@
 //              K/V come from a per-request 4-D tensor map over the request VA
 //              (d, token-in-chunk, (layer,K|V,head) block, chunk) whose chunk
 //              extent is ceil(kv_len/tpc): the TMA never touches unmapped VA.
-//   warp 9     MMA issuer (one thread), per 64-key block i and slot s:
-//                S_s(i)   = Q_s K_i^T   (SS: both operands in smem) -> TMEM
-//                O_s     += P_s(i) V_i  (TS: P read from TMEM, V MN-major smem)
-//              issued as S(i+1), PV(i): S(i+1) overwrites the buffer of P(i-1)
-//              only after the PV that consumed it (tcgen05.mma executes in
-//              issue order).
+//   warp 9     MMA issuer. Per slot s: S_s(0), then per key block j one group
+//                O_s  += P_s(j) V_j        (TS: P read from TMEM, V MN-major)
+//                S_s(j+1) = Q_s K_{j+1}^T  (SS)
+//              S_s(j+1) overwrites the columns of P_s(j) right after the PV
+//              that consumes it (tcgen05.mma executes in issue order). The
+//              whole warp walks the schedule (descriptors stay in uniform
+//              registers); one elected lane issues.
 //   warps 0-3  softmax slot 0;  warps 4-7  softmax slot 1. Thread <-> TMEM
 //              lane <-> query row: tcgen05.ld of S, causal + length mask, online
 //              softmax in the exp2 domain with a lazy running max (O and l are
@@ -35,10 +38,10 @@
 //              exact because numerator and denominator share the stale max),
 //              packed fp32x2 arithmetic, a quarter of the exponentials on the
 //              FMA pipe (polynomial) to offload MUFU, P -> TMEM as packed bf16
-//              over its S buffer, final O / l -> bf16 -> global.
+//              over the first 64 S columns, final O / l -> bf16 -> global.
 //
-// TMEM (512 columns): slot s has score buffers at 128 s + {0, 64} (64 columns
-// each; P(i) takes the first 32) and O at [256 + 128 s, 384 + 128 s).
+// TMEM (512 columns): slot s has S/P at [128 s, 128 s + 128) and O at
+// [256 + 128 s, 384 + 128 s).
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -51,9 +54,8 @@
 namespace vt {
 namespace pf {
 
-constexpr int BM = 128;
-constexpr int BN = 128;  // keys per K/V tile (TMA)
-constexpr int BS = 64;   // keys per score block (S double-buffered per slot)
+constexpr int BM = 128;  // query rows per slot
+constexpr int BN = 128;  // keys per K/V tile and per score block
 constexpr int D = 128;
 constexpr int kStages = 2;
 constexpr int kSlots = 2;
@@ -73,20 +75,11 @@ struct __align__(1024) Smem {
   uint64_t q_full;
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
-  uint64_t s_full[kSlots][2];
-  uint64_t p_full[kSlots][2];
+  uint64_t s_full[kSlots];
+  uint64_t p_full[kSlots];
   uint64_t o_done[kSlots];
   uint32_t tmem_base;
 };
-
-// D[tmem] (+)= A[tmem] * B[smem desc]   (A = P, 128 lanes x 16 bf16 keys)
-__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id,
-                                       uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(b), "r"(id), "r"(acc));
-}
 
 #define VT_R32(x)                                                                              \
   "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),          \
@@ -143,6 +136,17 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
 
+#ifdef VT_PF_TRACE
+// Debug timeline of CTA (0,0,0) (clock64): [slot][j][0]=S ready, [1]=P arrived;
+// mma[j][s]=group {PV_s(j), S_s(j+1)} issued.
+__device__ long long g_pf_trace_sm[2][64][2];
+__device__ long long g_pf_trace_mma[64][2];
+#define VT_TRACE(cond, dst) \
+  if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) dst = clock64();
+#else
+#define VT_TRACE(cond, dst)
+#endif
+
 struct Args {
   __nv_bfloat16* out;       // [B, n_new, Hq, D]
   const CUtensorMap* kv;    // [B] per-request maps
@@ -166,8 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int start = a.start[b];
   const int kv_len = start + a.n_new;
   const int q_last = min(a.n_new, (t + 1) * BM);  // exclusive, relative to start
-  const int n_sub = (start + q_last + BS - 1) / BS;  // 64-key score blocks
-  const int n_kv = (n_sub + 1) / 2;                  // 128-key K/V tiles
+  const int n_kv = (start + q_last + BN - 1) / BN;
   const int hk = h0 / (a.hq / a.hkv);
   const int blk_k = (a.layer * 2 + 0) * a.hkv + hk;
   const int blk_v = (a.layer * 2 + 1) * a.hkv + hk;
@@ -183,10 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.v_empty[i], 1);
     }
     for (int s = 0; s < kSlots; ++s) {
-      for (int u = 0; u < 2; ++u) {
-        mbar_init(&sm.s_full[s][u], 1);
-        mbar_init(&sm.p_full[s][u], 128);
-      }
+      mbar_init(&sm.s_full[s], 1);
+      mbar_init(&sm.p_full[s], 128);
       mbar_init(&sm.o_done[s], 1);
     }
     fence_mbar_init();
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp >= kSlots * 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
     if (warp == kTmaWarp) {
       // ------------------------------ TMA producer ------------------------------
       if (lane == 0) {
@@ -230,115 +231,104 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     } else if (warp == kMmaWarp) {
       // ------------------------------- MMA issuer -------------------------------
-      // Order: S(0); then per score block i: S(i+1) for every slot, PV(i) for
-      // every slot. S(i+1) lands in the TMEM buffer that held P(i-1), whose PV
-      // was issued one step earlier (tcgen05.mma runs in issue order). The
-      // whole warp walks the schedule so descriptors stay warp-uniform (uniform
-      // registers); one elected lane issues each MMA group and its commits.
-      constexpr uint32_t id_s = tc::idesc_bf16(BM, BS, false, false);
+      constexpr uint32_t id_s = tc::idesc_bf16(BM, BN, false, false);
       constexpr uint32_t id_pv = tc::idesc_bf16(BM, D, false, true);
+      constexpr uint32_t hi = tc::sdesc_hi(1024);  // SW128: 8-row groups 1 KiB apart
       // Descriptor address fields count 16 B units: a [.][64] bf16 tile half
-      // is 16 KiB = 1024 units, 64 keys = 512, one 16-element K step inside a
-      // SW128 row = 2, 16 keys of V = 128.
-      const uint64_t dq = tc::sdesc(sm.q[0][0], 16, 1024);
-      const uint64_t dk = tc::sdesc(sm.k[0][0], 16, 1024);
-      const uint64_t dv = tc::sdesc(sm.v[0][0], BN * 128, 1024);
-      auto issue_s = [&](int s, int i) {
-        const int st = (i >> 1) % kStages;
-        const uint32_t d = tmem + static_cast<uint32_t>(s * 2 * BS + (i & 1) * BS);
-        const uint64_t a0 = dq + static_cast<uint64_t>(s * 2048);
-        const uint64_t b0 = dk + static_cast<uint64_t>(st * 2048 + (i & 1) * 512);
-        if (tc::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint64_t off = static_cast<uint64_t>((kk >> 2) * 1024 + 2 * (kk & 3));
-            tc::mma(d, a0 + off, b0 + off, id_s, kk > 0 ? 1u : 0u);
-          }
-          tc::commit(&sm.s_full[s][i & 1]);
-        }
-        __syncwarp();
-      };
-      auto issue_pv = [&](int s, int i) {
-        const int st = (i >> 1) % kStages;
-        mbar_wait(&sm.p_full[s][i & 1], (i >> 1) & 1);
+      // is 16 KiB = 1024 units, one 16-element K step inside a SW128 row = 2,
+      // 16 keys of V = 128.
+      const uint32_t lq = tc::sdesc_lo(smem_u32(sm.q[0][0]), 16);
+      const uint32_t lk = tc::sdesc_lo(smem_u32(sm.k[0][0]), 16);
+      const uint32_t lv = tc::sdesc_lo(smem_u32(sm.v[0][0]), BN * 128);
+      auto wait_fence = [&](uint64_t* bar, uint32_t parity) {
+        mbar_wait(bar, parity);
         tc::fence_after();
+      };
+      auto mma_s = [&](int s, int j) {  // elected lane only
+        const uint32_t b0 = lk + static_cast<uint32_t>((j % kStages) * 2048);
+        const uint32_t a0 = lq + static_cast<uint32_t>(s * 2048);
+        const uint32_t d = tmem + static_cast<uint32_t>(s * BN);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = static_cast<uint32_t>((kk >> 2) * 1024 + 2 * (kk & 3));
+          tc::mma_ss(d, a0 + off, hi, b0 + off, hi, id_s, kk > 0 ? 1u : 0u);
+        }
+        tc::commit(&sm.s_full[s]);
+      };
+      auto mma_pv = [&](int s, int j) {  // elected lane only
+        const uint32_t b0 = lv + static_cast<uint32_t>((j % kStages) * 2048);
         const uint32_t d = tmem + kOCol + static_cast<uint32_t>(s * D);
-        const uint32_t p = tmem + static_cast<uint32_t>(s * 2 * BS + (i & 1) * BS);
-        const uint64_t b0 = dv + static_cast<uint64_t>(st * 2048 + (i & 1) * 512);
-        if (tc::elect_one()) {
+        const uint32_t p = tmem + static_cast<uint32_t>(s * BN);
 #pragma unroll
-          for (int kk = 0; kk < BS / 16; ++kk)
-            mma_ts(d, p + 8 * kk, b0 + static_cast<uint64_t>(kk * 128), id_pv,
-                   (i > 0 || kk > 0) ? 1u : 0u);
-          tc::commit(&sm.o_done[s]);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < BN / 16; ++kk)
+          tc::mma_ts(d, p + 8 * kk, b0 + static_cast<uint32_t>(kk * 128), hi, id_pv,
+                     (j > 0 || kk > 0) ? 1u : 0u);
+        tc::commit(&sm.o_done[s]);
       };
-      auto commit1 = [&](uint64_t* bar) {
-        if (tc::elect_one()) tc::commit(bar);
-        __syncwarp();
-      };
-      mbar_wait(&sm.q_full, 0);
-      mbar_wait(&sm.k_full[0], 0);
-      tc::fence_after();
-#pragma unroll
-      for (int s = 0; s < kSlots; ++s)
-        if (s < nslots) issue_s(s, 0);
-      if (n_sub == 1) commit1(&sm.k_empty[0]);
-      for (int i = 0; i < n_sub; ++i) {
-        const int nx = i + 1;
-        if (nx < n_sub) {
-          const int tile = nx >> 1;
-          if ((nx & 1) == 0) {
-            mbar_wait(&sm.k_full[tile % kStages], (tile / kStages) & 1);
-            tc::fence_after();
-          }
-#pragma unroll
-          for (int s = 0; s < kSlots; ++s)
-            if (s < nslots) issue_s(s, nx);
-          if ((nx & 1) == 1 || nx == n_sub - 1) commit1(&sm.k_empty[tile % kStages]);
-        }
-        const int tile = i >> 1;
-        if ((i & 1) == 0) mbar_wait(&sm.v_full[tile % kStages], (tile / kStages) & 1);
+      wait_fence(&sm.q_full, 0);
+      wait_fence(&sm.k_full[0], 0);
+      if (tc::elect_one()) {
 #pragma unroll
         for (int s = 0; s < kSlots; ++s)
-          if (s < nslots) issue_pv(s, i);
-        if ((i & 1) == 1 || i == n_sub - 1) commit1(&sm.v_empty[tile % kStages]);
+          if (s < nslots) mma_s(s, 0);
+        tc::commit(&sm.k_empty[0]);
       }
       __syncwarp();
+      for (int j = 0; j < n_kv; ++j) {
+        const bool more = j + 1 < n_kv;
+        mbar_wait(&sm.v_full[j % kStages], (j / kStages) & 1);
+        if (more) mbar_wait(&sm.k_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s) {
+          if (s < nslots) {
+            const bool last_slot = s == nslots - 1;
+            wait_fence(&sm.p_full[s], j & 1);
+            if (tc::elect_one()) {
+              mma_pv(s, j);
+              if (last_slot) tc::commit(&sm.v_empty[j % kStages]);
+              if (more) {
+                mma_s(s, j + 1);
+                if (last_slot) tc::commit(&sm.k_empty[(j + 1) % kStages]);
+              }
+            }
+            __syncwarp();
+            VT_TRACE(lane == 0 && j < 64, g_pf_trace_mma[j][s]);
+          }
+        }
+      }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
     if (warp / 4 < nslots) {
       // ------------------------------ softmax slot s ------------------------------
       const int s = warp / 4;
       const int quarter = warp & 3;  // TMEM lane quarter this warp may access
       const int row = quarter * 32 + lane;
       const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      const uint32_t s_addr = lane_addr + static_cast<uint32_t>(s * 2 * BS);
+      const uint32_t s_addr = lane_addr + static_cast<uint32_t>(s * BN);
       const uint32_t o_addr = lane_addr + kOCol + static_cast<uint32_t>(s * D);
       const int qpos = start + t * BM + row;  // absolute position of this query row
       const int qmin = start + t * BM;        // smallest query position of the tile
       float m_run = -INFINITY, l_run = 0.f;
       const float sl2 = a.scale_log2;
-      for (int i = 0; i < n_sub; ++i) {
-        const int kpos0 = i * BS;
-        const uint32_t sb = s_addr + static_cast<uint32_t>((i & 1) * BS);
-        mbar_wait(&sm.s_full[s][i & 1], (i >> 1) & 1);
+      for (int j = 0; j < n_kv; ++j) {
+        const int kpos0 = j * BN;
+        mbar_wait(&sm.s_full[s], j & 1);
         tc::fence_after();
-        float x[BS];
+        VT_TRACE(row == 0, g_pf_trace_sm[s][j & 63][0]);
+        float x[BN];
         {
-          uint32_t r[BS];
-          tmem_ld32(sb, r);
-          tmem_ld32(sb + 32, r + 32);
+          uint32_t r[BN];
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + 32 * c, r + 32 * c);
           tc::wait_ld();
 #pragma unroll
-          for (int k = 0; k < BS; ++k) x[k] = __uint_as_float(r[k]);
+          for (int k = 0; k < BN; ++k) x[k] = __uint_as_float(r[k]);
         }
-        if (kpos0 + BS - 1 > qmin || kpos0 + BS > kv_len) {
+        if (kpos0 + BN - 1 > qmin || kpos0 + BN > kv_len) {
           const int lim = min(qpos + 1, kv_len) - kpos0;  // keys [0, lim) are visible
 #pragma unroll
-          for (int k = 0; k < BS; ++k)
+          for (int k = 0; k < BN; ++k)
             if (k >= lim) x[k] = -INFINITY;
         }
         float mx;
@@ -347,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) m8[k] = fmaxf(x[k], x[k + 8]);
 #pragma unroll
-          for (int k = 16; k < BS; k += 16)
+          for (int k = 16; k < BN; k += 16)
 #pragma unroll
             for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(x[k + u], x[k + 8 + u]));
           mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
@@ -362,9 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 negm = make_float2(-m_use, -m_use);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
-        uint32_t pr[BS / 2];
+        uint32_t pr[BN / 2];
 #pragma unroll
-        for (int k = 0; k < BS / 2; ++k) {
+        for (int k = 0; k < BN / 2; ++k) {
           float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
           if ((k & 3) == kPolyLane) {
             e = ex2_poly2(e);
@@ -378,10 +368,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
         l_run = fmaf(l_run, alpha, a01.x + a01.y);
         m_run = m_new;
-        // P -> TMEM over the score buffer: column c = keys (2c, 2c+1) as bf16x2.
-        tmem_st32(sb, pr);
-        if (i >= 1 && __any_sync(0xffffffffu, grow)) {
-          mbar_wait(&sm.o_done[s], (i - 1) & 1);  // PV(i-1) done: O stable
+        // P -> TMEM over the first 64 S columns: column c = keys (2c, 2c+1) as bf16x2.
+        tmem_st32(s_addr, pr);
+        tmem_st32(s_addr + 32, pr + 32);
+        if (j >= 1 && __any_sync(0xffffffffu, grow)) {
+          // PV(j-1) is complete: S(j) was issued after it and has completed.
+          mbar_wait(&sm.o_done[s], (j - 1) & 1);
           tc::fence_after();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -394,15 +386,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         bool zeroed = false;
-        if (s == 0 && i == n_sub - 1 && (i | 1) * BS + BS > kv_len) {
+        if (s == 0 && j == n_kv - 1 && kpos0 + BN > kv_len) {
           // Rows past kv_len may hold stale/uninitialised bytes of the last
           // mapped chunk: zero them so 0 * NaN cannot reach the accumulator.
-          // (Earlier PVs read only rows below kv_len; slot 1's PV of this block
-          // is issued after slot 0's P arrives.)
-          const int tile = i >> 1;
-          const int st = tile % kStages;
-          mbar_wait(&sm.v_full[st], (tile / kStages) & 1);
-          if (tile * BN + row >= kv_len) {
+          // (Slot 1's PV of this tile is issued after slot 0's P arrives.)
+          const int st = j % kStages;
+          mbar_wait(&sm.v_full[st], (j / kStages) & 1);
+          if (kpos0 + row >= kv_len) {
             const uint4 z = make_uint4(0, 0, 0, 0);
             uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][0]) + row * 128);
             uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][1]) + row * 128);
@@ -417,14 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::wait_st();
         if (zeroed) fence_proxy_async_smem();
         tc::fence_before();
-        mbar_arrive(&sm.p_full[s][i & 1]);
+        mbar_arrive(&sm.p_full[s]);
+        VT_TRACE(row == 0, g_pf_trace_sm[s][j & 63][1]);
       }
-      // epilogue. o_done completes once per PV. S(n_sub-1) completing only
-      // proves PV(n_sub-3) done (S(i+1) is issued ahead of PV(i)), so step
-      // through the last two phases in order: a parity wait is only
-      // unambiguous one phase ahead.
-      if (n_sub >= 2) mbar_wait(&sm.o_done[s], (n_sub - 2) & 1);
-      mbar_wait(&sm.o_done[s], (n_sub - 1) & 1);
+      // epilogue: PV(n_kv-2) completed before S(n_kv-1); wait for the last PV.
+      mbar_wait(&sm.o_done[s], (n_kv - 1) & 1);
       tc::fence_after();
       const int tok = t * BM + row;
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -457,6 +444,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace vt
 
 using namespace vt::pf;
+
+#ifdef VT_PF_TRACE
+extern "C" int vt_prefill_trace(long long* out) {  // 2*64*2 + 64*2 values
+  cudaMemcpyFromSymbol(out, g_pf_trace_sm, sizeof(g_pf_trace_sm));
+  return cudaMemcpyFromSymbol(out + 2 * 64 * 2, g_pf_trace_mma, sizeof(g_pf_trace_mma));
+}
+#endif
 
 extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                                     const void* kv_maps, const int32_t* start, int32_t batch,

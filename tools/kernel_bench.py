@@ -120,20 +120,26 @@ def bench_decode(args, pk):
 
 
 def bench_prefill(args, pk):
-    L, hkv, hq, B, prefix, n_new = 32, 8, 32, 16, 2048, 512
-    cfg, dev, ops, sched, geo = stack(L, hkv, hq, 4096, 4096)
+    L, hkv, hq, B, prefix, n_new = 32, 8, 32, args.pf_batch, args.pf_prefix, args.pf_new
+    max_seq = max(4096, -(-(prefix + n_new) // 4096) * 4096)
+    cfg, dev, ops, sched, geo = stack(L, hkv, hq, max_seq, max(4096, B * max_seq // 16 + max_seq // 16))
     gen = torch.Generator(device="cuda").manual_seed(1)
     tpc = cfg.tokens_per_chunk
     base = [i % 251 for i in range(prefix)]
-    sched.create("donor", base)
-    sched.mark_prefilled("donor")
-    dev.wait()
-    fill(dev.va(sched.mem["donor"].vt.space.rng), sched.mem["donor"].vt.space.mapped_pages, geo, gen)
-    assert sched.prefix_record("donor")
+    if prefix:
+        sched.create("donor", base)
+        sched.mark_prefilled("donor")
+        dev.wait()
+        fill(dev.va(sched.mem["donor"].vt.space.rng), sched.mem["donor"].vt.space.mapped_pages, geo, gen)
+        assert sched.prefix_record("donor")
     vas = []
     for b in range(B):
-        hit = sched.prefix_match(f"t{b}", base + [7000 + b * 600 + k for k in range(n_new)])
-        assert hit is not None and hit[1].shared_tokens == prefix
+        toks = base + [7000 + b * 600 + k for k in range(n_new)]
+        if prefix:
+            hit = sched.prefix_match(f"t{b}", toks)
+            assert hit is not None and hit[1].shared_tokens == prefix
+        else:
+            sched.create(f"t{b}", toks)
         vas.append(dev.va(sched.mem[f"t{b}"].vt.space.rng))
     dev.wait()
     for b in range(B):
@@ -152,7 +158,7 @@ def bench_prefill(args, pk):
     flops = 4 * hq * 128 * (n_new * prefix + n_new * (n_new + 1) // 2) * B
     tf = flops / (ms * 1e-3) / 1e12
     dev.wait()
-    return [{"kernel": "prefill", "config": "cfg3 16 x (2048 shared + 512 new)", "us": round(ms * 1e3, 2),
+    return [{"kernel": "prefill", "config": f"{B} x ({prefix} shared + {n_new} new)", "us": round(ms * 1e3, 2),
              "flops": flops, "TFLOP/s": round(tf, 1),
              "frac_of_bf16_burst": round(tf / pk["bf16_tflops"], 4),
              "frac_of_bf16_sustained": round(tf / pk["bf16_tflops_sustained"], 4)}]
@@ -167,6 +173,9 @@ def main():
     ap.add_argument("--paths", type=lambda s: s.split(","), default=["tcgen05", "cuda_core"])
     ap.add_argument("--loop", action="store_true", help="time 32 back-to-back launches")
     ap.add_argument("--shape", choices=["8b", "70b"], default="8b")
+    ap.add_argument("--pf-batch", type=int, default=16, help="prefill: requests (config 3: 16)")
+    ap.add_argument("--pf-prefix", type=int, default=2048, help="prefill: shared prefix tokens")
+    ap.add_argument("--pf-new", type=int, default=512, help="prefill: new tokens per request")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     pk = peaks()
