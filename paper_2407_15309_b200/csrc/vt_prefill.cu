@@ -36,7 +36,7 @@
 //              softmax in the exp2 domain with a lazy running max (O and l are
 //              rescaled only when a row's max grows by more than 2^8, which is
 //              exact because numerator and denominator share the stale max),
-//              packed fp32x2 arithmetic, a quarter of the exponentials on the
+//              packed fp32x2 arithmetic, 3/8 of the exponentials on the
 //              FMA pipe (polynomial) to offload MUFU, P -> TMEM as packed bf16
 //              over the first 64 S columns, final O / l -> bf16 -> global.
 //
@@ -63,10 +63,13 @@ constexpr int kThreads = kSlots * 128 + 128;  // softmax WGs, then TMA/MMA WG
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kOCol = 256;
 constexpr float kRescaleLog2 = 8.0f;  // lazy max: rescale only when it grows by > 2^8
-#ifndef VT_PF_POLY_LANE
-#define VT_PF_POLY_LANE 3
+#ifndef VT_PF_POLY_MASK
+#define VT_PF_POLY_MASK 0x92
 #endif
-constexpr int kPolyLane = VT_PF_POLY_LANE;  // pair k with k % 4 == this: exp2 on the FMA pipe
+// Pair k of a row's scores takes exp2 on the FMA pipe (polynomial) when bit
+// (k % 8) of this mask is set (3 of 8 measured best on config 3: 1117 vs 1092
+// TFLOP/s for 2 of 8, 1015 for 4 of 8); the rest use MUFU.EX2.
+constexpr uint32_t kPolyMask = VT_PF_POLY_MASK;
 
 struct __align__(1024) Smem {
   __nv_bfloat16 q[kSlots][2][BM * 64];    // SW128 K-major: d 0-63 | d 64-127
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < BN / 2; ++k) {
           float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
-          if ((k & 3) == kPolyLane) {
+          if ((kPolyMask >> (k & 7)) & 1u) {
             e = ex2_poly2(e);
           } else {
             e.x = tc::ex2(e.x);
