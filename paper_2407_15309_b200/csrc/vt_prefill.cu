@@ -75,7 +75,7 @@ struct __align__(1024) Smem {
   __nv_bfloat16 q[kSlots][2][BM * 64];    // SW128 K-major: d 0-63 | d 64-127
   __nv_bfloat16 k[kStages][2][BN * 64];   // SW128 K-major (keys x d)
   __nv_bfloat16 v[kStages][2][BN * 64];   // SW128, read as MN-major B (d x keys)
-  uint64_t q_full;
+  uint64_t q_full, q_empty;
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[kSlots];
@@ -155,33 +155,49 @@ struct Args {
   const CUtensorMap* kv;    // [B] per-request maps
   const int32_t* start;     // [B]
   int32_t n_new, hq, hkv, tpc, layer, slots;
+  int32_t batch, pairs, n_qtiles, n_items;
   float scale_log2;
 };
 
+// Work item w -> (q tile, head pair, request). Longest q tiles first (a
+// tile's key count grows with t), pairs of one kv head adjacent so concurrent
+// CTAs share K/V tiles in L2; CTAs take items w = blockIdx.x + k * gridDim.x.
+struct Item {
+  int t, h0, b, start, kv_len, n_kv, blk_k, blk_v;
+};
+__device__ __forceinline__ Item item_of(int w, const Args& a) {
+  Item it;
+  const int per_t = a.pairs * a.batch;
+  it.t = a.n_qtiles - 1 - w / per_t;
+  const int r = w % per_t;
+  it.h0 = (r % a.pairs) * a.slots;
+  it.b = r / a.pairs;
+  it.start = a.start[it.b];
+  it.kv_len = it.start + a.n_new;
+  const int q_last = min(a.n_new, (it.t + 1) * BM);  // exclusive, relative to start
+  it.n_kv = (it.start + q_last + BN - 1) / BN;
+  const int hk = it.h0 / (a.hq / a.hkv);
+  it.blk_k = (a.layer * 2 + 0) * a.hkv + hk;
+  it.blk_v = (a.layer * 2 + 1) * a.hkv + hk;
+  return it;
+}
+
+// Persistent: one CTA per SM walks its work items; barrier phases and the K/V
+// ring run on per-CTA global counters (g = key blocks processed so far), so
+// the next item's Q and first K/V tiles load while the current item drains.
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap q_map, const Args a) {
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                       ~static_cast<uintptr_t>(1023));
-  const int n_qtiles = gridDim.x;
-  const int t = n_qtiles - 1 - static_cast<int>(blockIdx.x);  // longest tiles first
   const int nslots = a.slots;
-  const int h0 = blockIdx.y * nslots;
-  const int b = blockIdx.z;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int start = a.start[b];
-  const int kv_len = start + a.n_new;
-  const int q_last = min(a.n_new, (t + 1) * BM);  // exclusive, relative to start
-  const int n_kv = (start + q_last + BN - 1) / BN;
-  const int hk = h0 / (a.hq / a.hkv);
-  const int blk_k = (a.layer * 2 + 0) * a.hkv + hk;
-  const int blk_v = (a.layer * 2 + 1) * a.hkv + hk;
-  const CUtensorMap* kvmap = a.kv + b;
   constexpr int kTmaWarp = kSlots * 4, kMmaWarp = kSlots * 4 + 1;
 
   if (warp == kTmaWarp && lane == 0) {
     mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 1);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.k_full[i], 1);
       mbar_init(&sm.k_empty[i], 1);
@@ -207,28 +223,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------ TMA producer ------------------------------
       if (lane == 0) {
         tma_prefetch_desc(&q_map);
-        tma_prefetch_desc(kvmap);
         const uint64_t keep = l2_evict_last_policy();   // K/V re-read by the group's heads
         const uint64_t once = l2_evict_first_policy();
-        mbar_arrive_expect_tx(&sm.q_full, nslots * 2 * BM * 64 * 2);
-        for (int s = 0; s < nslots; ++s) {
-          tma_load_4d(sm.q[s][0], &q_map, &sm.q_full, 0, h0 + s, t * BM, b, once);
-          tma_load_4d(sm.q[s][1], &q_map, &sm.q_full, 64, h0 + s, t * BM, b, once);
-        }
-        for (int j = 0; j < n_kv; ++j) {
-          const int st = j % kStages;
-          const uint32_t ph = (j / kStages) & 1;
-          const int tok0 = j * BN;
-          const int c1 = tok0 % a.tpc;
-          const int c3 = tok0 / a.tpc;
-          if (j >= kStages) mbar_wait(&sm.k_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&sm.k_full[st], 2 * BN * 64 * 2);
-          tma_load_4d(sm.k[st][0], kvmap, &sm.k_full[st], 0, c1, blk_k, c3, keep);
-          tma_load_4d(sm.k[st][1], kvmap, &sm.k_full[st], 64, c1, blk_k, c3, keep);
-          if (j >= kStages) mbar_wait(&sm.v_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&sm.v_full[st], 2 * BN * 64 * 2);
-          tma_load_4d(sm.v[st][0], kvmap, &sm.v_full[st], 0, c1, blk_v, c3, keep);
-          tma_load_4d(sm.v[st][1], kvmap, &sm.v_full[st], 64, c1, blk_v, c3, keep);
+        int g = 0;  // K/V tiles loaded so far
+        int n = 0;  // items so far
+        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++n) {
+          const Item it = item_of(w, a);
+          const CUtensorMap* kvmap = a.kv + it.b;
+          if (n >= 1) mbar_wait(&sm.q_empty, (n - 1) & 1);  // last S of the previous item done
+          mbar_arrive_expect_tx(&sm.q_full, nslots * 2 * BM * 64 * 2);
+          for (int s = 0; s < nslots; ++s) {
+            tma_load_4d(sm.q[s][0], &q_map, &sm.q_full, 0, it.h0 + s, it.t * BM, it.b, once);
+            tma_load_4d(sm.q[s][1], &q_map, &sm.q_full, 64, it.h0 + s, it.t * BM, it.b, once);
+          }
+          for (int j = 0; j < it.n_kv; ++j, ++g) {
+            const int st = g % kStages;
+            const uint32_t ph = (g / kStages) & 1;
+            const int tok0 = j * BN;
+            const int c1 = tok0 % a.tpc;
+            const int c3 = tok0 / a.tpc;
+            if (g >= kStages) mbar_wait(&sm.k_empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&sm.k_full[st], 2 * BN * 64 * 2);
+            tma_load_4d(sm.k[st][0], kvmap, &sm.k_full[st], 0, c1, it.blk_k, c3, keep);
+            tma_load_4d(sm.k[st][1], kvmap, &sm.k_full[st], 64, c1, it.blk_k, c3, keep);
+            if (g >= kStages) mbar_wait(&sm.v_empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&sm.v_full[st], 2 * BN * 64 * 2);
+            tma_load_4d(sm.v[st][0], kvmap, &sm.v_full[st], 0, c1, it.blk_v, c3, keep);
+            tma_load_4d(sm.v[st][1], kvmap, &sm.v_full[st], 64, c1, it.blk_v, c3, keep);
+          }
         }
       }
       __syncwarp();
@@ -247,8 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar, parity);
         tc::fence_after();
       };
-      auto mma_s = [&](int s, int j) {  // elected lane only
-        const uint32_t b0 = lk + static_cast<uint32_t>((j % kStages) * 2048);
+      auto mma_s = [&](int s, int g) {  // elected lane only; g = global tile index
+        const uint32_t b0 = lk + static_cast<uint32_t>((g % kStages) * 2048);
         const uint32_t a0 = lq + static_cast<uint32_t>(s * 2048);
         const uint32_t d = tmem + static_cast<uint32_t>(s * BN);
 #pragma unroll
@@ -258,44 +280,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::commit(&sm.s_full[s]);
       };
-      auto mma_pv = [&](int s, int j) {  // elected lane only
-        const uint32_t b0 = lv + static_cast<uint32_t>((j % kStages) * 2048);
+      auto mma_pv = [&](int s, int g, bool first) {  // elected lane only
+        const uint32_t b0 = lv + static_cast<uint32_t>((g % kStages) * 2048);
         const uint32_t d = tmem + kOCol + static_cast<uint32_t>(s * D);
         const uint32_t p = tmem + static_cast<uint32_t>(s * BN);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
           tc::mma_ts(d, p + 8 * kk, b0 + static_cast<uint32_t>(kk * 128), hi, id_pv,
-                     (j > 0 || kk > 0) ? 1u : 0u);
+                     (!first || kk > 0) ? 1u : 0u);
         tc::commit(&sm.o_done[s]);
       };
-      wait_fence(&sm.q_full, 0);
-      wait_fence(&sm.k_full[0], 0);
-      if (tc::elect_one()) {
+      int g = 0, n = 0;
+      for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++n) {
+        const int n_kv = item_of(w, a).n_kv;
+        // S(0) of every slot; its S buffer was last read by the previous
+        // item's final PV, issued before (in-order).
+        wait_fence(&sm.q_full, n & 1);
+        wait_fence(&sm.k_full[g % kStages], (g / kStages) & 1);
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s)
-          if (s < nslots) mma_s(s, 0);
-        tc::commit(&sm.k_empty[0]);
-      }
-      __syncwarp();
-      for (int j = 0; j < n_kv; ++j) {
-        const bool more = j + 1 < n_kv;
-        mbar_wait(&sm.v_full[j % kStages], (j / kStages) & 1);
-        if (more) mbar_wait(&sm.k_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+          for (int s = 0; s < kSlots; ++s)
+            if (s < nslots) mma_s(s, g);
+          tc::commit(&sm.k_empty[g % kStages]);
+          if (n_kv == 1) tc::commit(&sm.q_empty);
+        }
+        __syncwarp();
+        for (int j = 0; j < n_kv; ++j, ++g) {
+          const bool more = j + 1 < n_kv;
+          mbar_wait(&sm.v_full[g % kStages], (g / kStages) & 1);
+          if (more) mbar_wait(&sm.k_full[(g + 1) % kStages], ((g + 1) / kStages) & 1);
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
-          if (s < nslots) {
-            const bool last_slot = s == nslots - 1;
-            wait_fence(&sm.p_full[s], j & 1);
-            if (tc::elect_one()) {
-              mma_pv(s, j);
-              if (last_slot) tc::commit(&sm.v_empty[j % kStages]);
-              if (more) {
-                mma_s(s, j + 1);
-                if (last_slot) tc::commit(&sm.k_empty[(j + 1) % kStages]);
+          for (int s = 0; s < kSlots; ++s) {
+            if (s < nslots) {
+              const bool last_slot = s == nslots - 1;
+              wait_fence(&sm.p_full[s], g & 1);
+              if (tc::elect_one()) {
+                mma_pv(s, g, j == 0);
+                if (last_slot) tc::commit(&sm.v_empty[g % kStages]);
+                if (more) {
+                  mma_s(s, g + 1);
+                  if (last_slot) {
+                    tc::commit(&sm.k_empty[(g + 1) % kStages]);
+                    if (j + 2 == n_kv) tc::commit(&sm.q_empty);  // the item's last S
+                  }
+                }
               }
+              __syncwarp();
             }
-            __syncwarp();
-            VT_TRACE(lane == 0 && j < 64, g_pf_trace_mma[j][s]);
           }
         }
       }
@@ -310,130 +341,135 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t s_addr = lane_addr + static_cast<uint32_t>(s * BN);
       const uint32_t o_addr = lane_addr + kOCol + static_cast<uint32_t>(s * D);
-      const int qpos = start + t * BM + row;  // absolute position of this query row
-      const int qmin = start + t * BM;        // smallest query position of the tile
-      float m_run = -INFINITY, l_run = 0.f;
       const float sl2 = a.scale_log2;
-      for (int j = 0; j < n_kv; ++j) {
-        const int kpos0 = j * BN;
-        mbar_wait(&sm.s_full[s], j & 1);
-        tc::fence_after();
-        VT_TRACE(row == 0, g_pf_trace_sm[s][j & 63][0]);
-        float x[BN];
-        {
-          uint32_t r[BN];
-#pragma unroll
-          for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + 32 * c, r + 32 * c);
-          tc::wait_ld();
-#pragma unroll
-          for (int k = 0; k < BN; ++k) x[k] = __uint_as_float(r[k]);
-        }
-        if (kpos0 + BN - 1 > qmin || kpos0 + BN > kv_len) {
-          const int lim = min(qpos + 1, kv_len) - kpos0;  // keys [0, lim) are visible
-#pragma unroll
-          for (int k = 0; k < BN; ++k)
-            if (k >= lim) x[k] = -INFINITY;
-        }
-        float mx;
-        {
-          float m8[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) m8[k] = fmaxf(x[k], x[k + 8]);
-#pragma unroll
-          for (int k = 16; k < BN; k += 16)
-#pragma unroll
-            for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(x[k + u], x[k + 8 + u]));
-          mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                     fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        }
-        const float mx_s = mx * sl2;
-        const bool grow = mx_s > m_run + kRescaleLog2;  // false while both are -inf
-        const float m_new = grow ? mx_s : m_run;
-        const float alpha = grow ? tc::ex2(m_run - m_new) : 1.f;
-        const float m_use = m_new == -INFINITY ? 0.f : m_new;
-        const float2 sl2v = make_float2(sl2, sl2);
-        const float2 negm = make_float2(-m_use, -m_use);
-        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                         make_float2(0.f, 0.f)};
-        uint32_t pr[BN / 2];
-#pragma unroll
-        for (int k = 0; k < BN / 2; ++k) {
-          float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
-          if ((kPolyMask >> (k & 7)) & 1u) {
-            e = ex2_poly2(e);
-          } else {
-            e.x = tc::ex2(e.x);
-            e.y = tc::ex2(e.y);
-          }
-          acc[k & 3] = __fadd2_rn(acc[k & 3], e);
-          pr[k] = pack_bf16(e.x, e.y);
-        }
-        const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
-        l_run = fmaf(l_run, alpha, a01.x + a01.y);
-        m_run = m_new;
-        // P -> TMEM over the first 64 S columns: column c = keys (2c, 2c+1) as bf16x2.
-        tmem_st32(s_addr, pr);
-        tmem_st32(s_addr + 32, pr + 32);
-        if (j >= 1 && __any_sync(0xffffffffu, grow)) {
-          // PV(j-1) is complete: S(j) was issued after it and has completed.
-          mbar_wait(&sm.o_done[s], (j - 1) & 1);
+      int g = 0;  // key blocks processed so far (barrier phases)
+      for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
+        const Item it = item_of(w, a);
+        const int qpos = it.start + it.t * BM + row;  // absolute position of this query row
+        const int qmin = it.start + it.t * BM;        // smallest query position of the tile
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < it.n_kv; ++j, ++g) {
+          const int kpos0 = j * BN;
+          mbar_wait(&sm.s_full[s], g & 1);
           tc::fence_after();
+          float x[BN];
+          {
+            uint32_t r[BN];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(o_addr + 32 * c, r);
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + 32 * c, r + 32 * c);
             tc::wait_ld();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
-            tmem_st32(o_addr + 32 * c, r);
+            for (int k = 0; k < BN; ++k) x[k] = __uint_as_float(r[k]);
           }
-        }
-        bool zeroed = false;
-        if (s == 0 && j == n_kv - 1 && kpos0 + BN > kv_len) {
-          // Rows past kv_len may hold stale/uninitialised bytes of the last
-          // mapped chunk: zero them so 0 * NaN cannot reach the accumulator.
-          // (Slot 1's PV of this tile is issued after slot 0's P arrives.)
-          const int st = j % kStages;
-          mbar_wait(&sm.v_full[st], (j / kStages) & 1);
-          if (kpos0 + row >= kv_len) {
-            const uint4 z = make_uint4(0, 0, 0, 0);
-            uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][0]) + row * 128);
-            uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][1]) + row * 128);
+          if (kpos0 + BN - 1 > qmin || kpos0 + BN > it.kv_len) {
+            const int lim = min(qpos + 1, it.kv_len) - kpos0;  // keys [0, lim) are visible
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              r0[c] = z;
-              r1[c] = z;
+            for (int k = 0; k < BN; ++k)
+              if (k >= lim) x[k] = -INFINITY;
+          }
+          float mx;
+          {
+            float m8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m8[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+            for (int k = 16; k < BN; k += 16)
+#pragma unroll
+              for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(x[k + u], x[k + 8 + u]));
+            mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          }
+          const float mx_s = mx * sl2;
+          const bool grow = mx_s > m_run + kRescaleLog2;  // false while both are -inf
+          const float m_new = grow ? mx_s : m_run;
+          const float alpha = grow ? tc::ex2(m_run - m_new) : 1.f;
+          const float m_use = m_new == -INFINITY ? 0.f : m_new;
+          const float2 sl2v = make_float2(sl2, sl2);
+          const float2 negm = make_float2(-m_use, -m_use);
+          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+          uint32_t pr[BN / 2];
+#pragma unroll
+          for (int k = 0; k < BN / 2; ++k) {
+            float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
+            if ((kPolyMask >> (k & 7)) & 1u) {
+              e = ex2_poly2(e);
+            } else {
+              e.x = tc::ex2(e.x);
+              e.y = tc::ex2(e.y);
+            }
+            acc[k & 3] = __fadd2_rn(acc[k & 3], e);
+            pr[k] = pack_bf16(e.x, e.y);
+          }
+          const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+          l_run = fmaf(l_run, alpha, a01.x + a01.y);
+          m_run = m_new;
+          // P -> TMEM over the first 64 S columns: column c = keys (2c, 2c+1) as bf16x2.
+          tmem_st32(s_addr, pr);
+          tmem_st32(s_addr + 32, pr + 32);
+          if (j >= 1 && __any_sync(0xffffffffu, grow)) {
+            // PV(j-1) is complete: S(j) was issued after it and has completed.
+            mbar_wait(&sm.o_done[s], (g - 1) & 1);
+            tc::fence_after();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t r[32];
+              tmem_ld32(o_addr + 32 * c, r);
+              tc::wait_ld();
+#pragma unroll
+              for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
+              tmem_st32(o_addr + 32 * c, r);
             }
           }
-          zeroed = true;
+          bool zeroed = false;
+          if (s == 0 && j == it.n_kv - 1 && kpos0 + BN > it.kv_len) {
+            // Rows past kv_len may hold stale/uninitialised bytes of the last
+            // mapped chunk: zero them so 0 * NaN cannot reach the accumulator.
+            // (Slot 1's PV of this tile is issued after slot 0's P arrives.)
+            const int st = g % kStages;
+            mbar_wait(&sm.v_full[st], (g / kStages) & 1);
+            if (kpos0 + row >= it.kv_len) {
+              const uint4 z = make_uint4(0, 0, 0, 0);
+              uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][0]) + row * 128);
+              uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][1]) + row * 128);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                r0[c] = z;
+                r1[c] = z;
+              }
+            }
+            zeroed = true;
+          }
+          tc::wait_st();
+          if (zeroed) fence_proxy_async_smem();
+          tc::fence_before();
+          mbar_arrive(&sm.p_full[s]);
         }
-        tc::wait_st();
-        if (zeroed) fence_proxy_async_smem();
+        // epilogue: PV(n_kv-2) completed before S(n_kv-1); wait for the last PV.
+        mbar_wait(&sm.o_done[s], (g - 1) & 1);
+        tc::fence_after();
+        const int tok = it.t * BM + row;
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        __nv_bfloat16* dst =
+            a.out + ((static_cast<int64_t>(it.b) * a.n_new + tok) * a.hq + (it.h0 + s)) * D;
+        uint32_t r[D];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(o_addr + 32 * c, r + 32 * c);
+        tc::wait_ld();
+        if (tok < a.n_new) {
+#pragma unroll
+          for (int k = 0; k < D; k += 8) {
+            uint4 w4;
+            w4.x = pack_bf16(__uint_as_float(r[k + 0]) * inv, __uint_as_float(r[k + 1]) * inv);
+            w4.y = pack_bf16(__uint_as_float(r[k + 2]) * inv, __uint_as_float(r[k + 3]) * inv);
+            w4.z = pack_bf16(__uint_as_float(r[k + 4]) * inv, __uint_as_float(r[k + 5]) * inv);
+            w4.w = pack_bf16(__uint_as_float(r[k + 6]) * inv, __uint_as_float(r[k + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + k) = w4;
+          }
+        }
+        // O is read: the next item's PV(0) (acc = 0) may overwrite it. That
+        // PV waits for this warpgroup's next P, which comes after this point.
         tc::fence_before();
-        mbar_arrive(&sm.p_full[s]);
-        VT_TRACE(row == 0, g_pf_trace_sm[s][j & 63][1]);
-      }
-      // epilogue: PV(n_kv-2) completed before S(n_kv-1); wait for the last PV.
-      mbar_wait(&sm.o_done[s], (n_kv - 1) & 1);
-      tc::fence_after();
-      const int tok = t * BM + row;
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      __nv_bfloat16* dst =
-          a.out + ((static_cast<int64_t>(b) * a.n_new + tok) * a.hq + (h0 + s)) * D;
-      uint32_t r[D];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(o_addr + 32 * c, r + 32 * c);
-      tc::wait_ld();
-      if (tok < a.n_new) {
-#pragma unroll
-        for (int k = 0; k < D; k += 8) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(r[k + 0]) * inv, __uint_as_float(r[k + 1]) * inv);
-          w.y = pack_bf16(__uint_as_float(r[k + 2]) * inv, __uint_as_float(r[k + 3]) * inv);
-          w.z = pack_bf16(__uint_as_float(r[k + 4]) * inv, __uint_as_float(r[k + 5]) * inv);
-          w.w = pack_bf16(__uint_as_float(r[k + 6]) * inv, __uint_as_float(r[k + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + k) = w;
-        }
       }
     }
   }
@@ -480,6 +516,10 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   a.tpc = g->tokens_per_chunk;
   a.layer = layer;
   a.slots = group % kSlots == 0 ? kSlots : 1;  // a pair never straddles two kv heads
+  a.batch = batch;
+  a.pairs = g->q_heads / a.slots;
+  a.n_qtiles = (n_new + BM - 1) / BM;
+  a.n_items = a.n_qtiles * a.pairs * batch;
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t smem = sizeof(Smem) + 1024;
   static bool attr = false;
@@ -488,7 +528,13 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
                          static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid((n_new + BM - 1) / BM, g->q_heads / a.slots, batch);
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = a.n_items < n_sm ? a.n_items : n_sm;  // persistent: one CTA per SM
   prefill_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(qmap, a);
   return cudaGetLastError();
 }
