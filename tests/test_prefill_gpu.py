@@ -67,6 +67,10 @@ CASES = {
     "ragged_prefix_100_new_200": (32, 8, 32, 100, 200, 2, 1024),
     "toy_mha_tpc512": (1, 8, 8, 1024, 300, 2, 4096),
     "gqa8_tpc128": (16, 2, 16, 640, 130, 1, 2048),
+    # more work items than SMs: every persistent CTA walks several items, so
+    # barrier phases and the K/V ring carry across items
+    "persistent_multi_item_gqa4": (32, 8, 32, 300, 700, 12, 2048),
+    "persistent_multi_item_mha": (1, 8, 8, 512, 1100, 8, 4096),
 }
 
 
