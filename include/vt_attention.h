@@ -93,6 +93,21 @@ int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                          const void* kv_maps, const int32_t* start, int32_t batch,
                          int32_t n_new, float scale, void* out, void* stream);
 
+/* Fused QKV projection + KV append, tcgen05/TMA with
+ * split-K (fp32 partials in a library-owned workspace, last slice reduces):
+ *   qkv = x . W^T    x [n_tokens, hidden] bf16, W [(Hq+2Hkv)*head_dim, hidden]
+ *                    bf16 (nn.Linear layout), fp32 accumulate
+ * Q rows -> q_out [n_tokens, q_heads, head_dim] bf16; K and V rows are written
+ * straight into request tok_req[t]'s VA (kv_va[tok_req[t]]) at token position
+ * tok_pos[t] of `layer`, in the vt_kv_append layout (the page must be mapped:
+ * the manager's extend ticket was waited on, kvsim/scheduler.py:189-205).
+ * hidden % 64 == 0. split_k <= 0 picks the K split that fills the SMs.
+ *   tok_req, tok_pos : [n_tokens] i32 (device);  kv_va : [n_req] u64 (device) */
+int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x, const void* w,
+                  int32_t hidden, int32_t n_tokens, const int32_t* tok_req,
+                  const int32_t* tok_pos, const uint64_t* kv_va, void* q_out, int32_t split_k,
+                  void* stream);
+
 /* Number of kernel launches the last call on this thread issued (bench
  * accounting of "gpu_launches"). */
 int32_t vt_attn_last_launches(void);

@@ -53,6 +53,9 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_prefill_attention.restype = c_int
         lib.vt_kv_tensor_maps.argtypes = [POINTER(_Geo), P, P, c_int32, P]
         lib.vt_kv_tensor_maps.restype = c_int
+        lib.vt_qkv_append.argtypes = [POINTER(_Geo), c_int32, P, P, c_int32, c_int32, P, P, P, P,
+                                      c_int32, P]
+        lib.vt_qkv_append.restype = c_int
         lib.vt_attn_last_launches.argtypes = []
         lib.vt_attn_last_launches.restype = c_int32
         _lib = lib
@@ -61,7 +64,8 @@ def attn_lib() -> ctypes.CDLL:
 
 ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_paged",
                 "vt_decode_workspace_bytes", "vt_kv_append",
-                "vt_kv_tensor_maps", "vt_prefill_attention", "vt_attn_last_launches")
+                "vt_kv_tensor_maps", "vt_prefill_attention", "vt_qkv_append",
+                "vt_attn_last_launches")
 
 
 def _geo(g: KVGeometry) -> _Geo:
@@ -166,6 +170,31 @@ def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, kv_va: torch.Tensor,
                                  v_new.data_ptr(), kv_va.data_ptr(), positions.data_ptr(), B,
                                  _stream(stream))
     _check(rc, "vt_kv_append")
+
+
+def qkv_append(x: torch.Tensor, w_qkv: torch.Tensor, tok_req: torch.Tensor,
+               tok_pos: torch.Tensor, kv_va: torch.Tensor, geo: KVGeometry, layer: int,
+               q_out: torch.Tensor | None = None, split_k: int = 0,
+               stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Fused QKV projection + KV append (include/vt_attention.h vt_qkv_append).
+
+    x ``[T, hidden]`` bf16, w_qkv ``[(Hq + 2 Hkv) * d, hidden]`` bf16. Returns q
+    ``[T, Hq, d]``; K/V of token t land in the cache of request ``tok_req[t]``
+    at position ``tok_pos[t]`` of ``layer`` (its page must already be mapped)."""
+    T, hidden = x.shape
+    feats = (geo.q_heads + 2 * geo.kv_heads) * geo.head_dim
+    if x.dtype != torch.bfloat16 or w_qkv.dtype != torch.bfloat16 or tuple(w_qkv.shape) != (feats, hidden):
+        raise ValueError(f"x must be bf16 [T, hidden], w_qkv bf16 [{feats}, hidden]")
+    if not (x.is_contiguous() and w_qkv.is_contiguous()):
+        raise ValueError("x and w_qkv must be contiguous")
+    if q_out is None:
+        q_out = torch.empty(T, geo.q_heads, geo.head_dim, dtype=torch.bfloat16, device=x.device)
+    _need_cuda(x, w_qkv, tok_req, tok_pos, kv_va, q_out)
+    rc = attn_lib().vt_qkv_append(ctypes.byref(_geo(geo)), layer, x.data_ptr(), w_qkv.data_ptr(),
+                                  hidden, T, tok_req.data_ptr(), tok_pos.data_ptr(),
+                                  kv_va.data_ptr(), q_out.data_ptr(), split_k, _stream(stream))
+    _check(rc, "vt_qkv_append")
+    return q_out
 
 
 def kv_tensor_maps(va: list[int], n_tokens: list[int], geo: KVGeometry,

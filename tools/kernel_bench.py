@@ -70,6 +70,33 @@ def timed(fn, iters, warmup):
     return statistics.median(ts), ts
 
 
+def timed_graph(fn, reps=20, iters=10):
+    """Device time per call of `fn`, launched from a CUDA graph of `reps` calls
+    (no host enqueue latency in the measurement)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / reps)
+    return statistics.median(ts), ts
+
+
 def bench_decode(args, pk):
     # 8b: Llama-3-8B (G=4, tpc 16); 70b: one 16-layer group of Llama-2-70B (G=8, tpc 32)
     L, hkv, hq, B, ctx = (32, 8, 32, 64, 4096) if args.shape == "8b" else (16, 8, 64, 64, 4096)
@@ -164,6 +191,59 @@ def bench_prefill(args, pk):
              "frac_of_bf16_sustained": round(tf / pk["bf16_tflops_sustained"], 4)}]
 
 
+def bench_qkv(args, pk):
+    """Fused QKV projection + KV append, Llama-3-8B decode step shape (one
+    layer): x [B, 4096] @ W_qkv[6144, 4096]^T, K/V written into the cache.
+    Baseline in the same run: cuBLAS GEMM (torch) + vt_kv_append (unfused).
+    Both timed as device time from a CUDA graph of 20 calls (4 weights of
+    50 MB rotate, so W is never L2-resident)."""
+    from paper_2407_15309_b200.attention import kv_append, qkv_append
+    L, hkv, hq, hidden = 32, 8, 32, 4096
+    res = []
+    for B in args.qkv_batch:
+        cfg, dev, ops, sched, geo = stack(L, hkv, hq, 4096, 4096)
+        vas = []
+        for b in range(B):
+            sched.create(f"r{b}", [1] * 100)
+            sched.mark_prefilled(f"r{b}")
+            sched.extend(f"r{b}", 101)
+            vas.append(dev.va(sched.mem[f"r{b}"].vt.space.rng))
+        dev.wait()
+        kv_va = torch.tensor(vas, dtype=torch.int64, device="cuda")
+        tok_req = torch.arange(B, dtype=torch.int32, device="cuda")
+        tok_pos = torch.full((B,), 100, dtype=torch.int32, device="cuda")
+        feats = (hq + 2 * hkv) * 128
+        ws = [(torch.randn(feats, hidden, device="cuda") / 64).to(torch.bfloat16) for _ in range(4)]
+        x = torch.randn(B, hidden, device="cuda").to(torch.bfloat16)
+        q = torch.empty(B, hq, 128, dtype=torch.bfloat16, device="cuda")
+        nbytes = feats * hidden * 2 + B * hidden * 2 + B * feats * 2
+        lay = [0]
+        for split in args.qkv_split:
+            def fn():
+                qkv_append(x, ws[lay[0] % 4], tok_req, tok_pos, kv_va, geo, lay[0] % L, q_out=q,
+                           split_k=split)
+                lay[0] += 1  # 4 weights x 50 MB rotate: never L2-resident
+            ms, _ = timed_graph(fn)
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            res.append({"kernel": "qkv_append (fused)", "config": f"llama3-8b B{B}", "split_k": split,
+                        "us": round(ms * 1e3, 2), "bytes": nbytes, "GB/s": round(gbs, 1),
+                        "frac_of_hbm": round(gbs / pk["hbm_gbs"], 4)})
+
+        def unfused():
+            y = x @ ws[lay[0] % 4].T
+            k = y[:, hq * 128:(hq + hkv) * 128].reshape(1, B, hkv, 128)
+            v = y[:, (hq + hkv) * 128:].reshape(1, B, hkv, 128)
+            kv_append(k.contiguous(), v.contiguous(), kv_va, tok_pos, geo, layer_begin=lay[0] % L)
+            lay[0] += 1
+        ms, _ = timed_graph(unfused)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        res.append({"kernel": "cuBLAS GEMM + vt_kv_append (unfused)", "config": f"llama3-8b B{B}",
+                    "us": round(ms * 1e3, 2), "GB/s": round(gbs, 1),
+                    "frac_of_hbm": round(gbs / pk["hbm_gbs"], 4)})
+        dev.wait()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="decode,prefill")
@@ -173,6 +253,8 @@ def main():
     ap.add_argument("--paths", type=lambda s: s.split(","), default=["tcgen05", "cuda_core"])
     ap.add_argument("--loop", action="store_true", help="time 32 back-to-back launches")
     ap.add_argument("--shape", choices=["8b", "70b"], default="8b")
+    ap.add_argument("--qkv-batch", type=lambda s: [int(x) for x in s.split(",")], default=[64])
+    ap.add_argument("--qkv-split", type=lambda s: [int(x) for x in s.split(",")], default=[0])
     ap.add_argument("--pf-batch", type=int, default=16, help="prefill: requests (config 3: 16)")
     ap.add_argument("--pf-prefix", type=int, default=2048, help="prefill: shared prefix tokens")
     ap.add_argument("--pf-new", type=int, default=512, help="prefill: new tokens per request")
@@ -184,6 +266,8 @@ def main():
         out += bench_decode(args, pk)
     if "prefill" in args.which:
         out += bench_prefill(args, pk)
+    if "qkv" in args.which:
+        out += bench_qkv(args, pk)
     for r in out:
         print(json.dumps(r))
 
