@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--premap", action="store_true",
                     help="map every chunk the run will need up front (config-5 comparison)")
     ap.add_argument("--no-prefill", action="store_true", help="skip the config-3 prefill probe")
+    ap.add_argument("--no-qkv", action="store_true",
+                    help="skip the fused QKV-projection + KV-append probe")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N untimed steps only (for ncu), print nothing")
     return ap.parse_args()
@@ -499,6 +501,9 @@ def run_ours(args, world, rank, local):
     prefill = None
     if rank == 0 and not args.no_prefill and args.config == "llama3-8b-decode":
         prefill = prefill_probe()
+    qkv = None
+    if rank == 0 and not args.no_qkv and args.config == "llama3-8b-decode":
+        qkv = qkv_probe()
 
     if rank == 0:
         ext = sorted(wl.extend_ns) or [0]
@@ -562,6 +567,7 @@ def run_ours(args, world, rank, local):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "prefill_cfg3": prefill,
+            "qkv_append": qkv,
             "premapped": bool(args.premap),
             "clocks": clocks.summary(),
         }
@@ -635,6 +641,96 @@ def prefill_probe(iters: int = 8) -> dict:
             "tflops": round(tf, 1), "frac_of_bf16_sustained": round(tf / pk["bf16_tflops_sustained"], 4),
             "frac_of_bf16_burst": round(tf / pk["bf16_tflops"], 4),
             "kernel": "vt::pf::prefill_kernel (tcgen05/TMEM/TMA)", "launches": last_launches()}
+
+
+# ---------------------------------------------- fused QKV + KV append probe --
+def qkv_probe(layers: int = 32) -> dict:
+    """SURVEY.md §8(f) row 2 at the config-2 shape: per layer, the new token
+    of each of 64 requests goes through the fused QKV projection
+    (x [64, 4096] . W_qkv[6144, 4096]^T, tcgen05) whose epilogue writes K/V
+    straight into each request's vTensor VA at token_count. Timed as device
+    time of a CUDA graph of 32 layers (32 distinct 50 MB weights: never
+    L2-resident), next to the unfused path (cuBLAS GEMM + vt_kv_append)."""
+    import torch
+
+    import paper_2407_15309_b200 as vt
+    from paper_2407_15309_b200.attention import kv_append, qkv_append
+    from paper_2407_15309_b200.kv_layout import KVGeometry
+
+    hkv, hq, hidden, B = 8, 32, 4096, 64
+    cfg = vt.SimConfig(capacity_bytes=8 * GIB, chunk_size_bytes=2 * MIB, weights_bytes=0,
+                       geometry=vt.ModelGeometry(layers, hkv, 128, 2), max_seq_len=4096,
+                       initial_alloc_tokens=0)
+    dev = vt.VirtualMemoryDevice(vt.DeviceConfig(cfg.capacity_bytes, cfg.chunk_size_bytes),
+                                 cuda_ordinal=torch.cuda.current_device())
+    sched = vt.VTensorScheduler(vt.VTensorOps(dev, vt.TensorPool(cfg.tokens_per_chunk), cfg))
+    geo = KVGeometry.from_config(cfg, hq)
+    vas = []
+    for b in range(B):
+        sched.create(f"r{b}", [1] * (100 + b))
+        sched.mark_prefilled(f"r{b}")
+        sched.extend(f"r{b}", 101 + b)
+        vas.append(dev.va(sched.mem[f"r{b}"].vt.space.rng))
+    dev.wait()
+    kv_va = torch.tensor(vas, dtype=torch.int64, device="cuda")
+    tok_req = torch.arange(B, dtype=torch.int32, device="cuda")
+    tok_pos = torch.arange(100, 100 + B, dtype=torch.int32, device="cuda")
+    feats = (hq + 2 * hkv) * 128
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    ws = [(torch.randn(feats, hidden, generator=gen, device="cuda") / 64).to(torch.bfloat16)
+          for _ in range(layers)]
+    x = torch.randn(B, hidden, generator=gen, device="cuda").to(torch.bfloat16)
+    q = torch.empty(B, hq, 128, dtype=torch.bfloat16, device="cuda")
+
+    def fused():
+        for l in range(layers):
+            qkv_append(x, ws[l], tok_req, tok_pos, kv_va, geo, l, q_out=q)
+
+    def unfused():
+        for l in range(layers):
+            y = x @ ws[l].T
+            kv_append(y[:, hq * 128:(hq + hkv) * 128].reshape(1, B, hkv, 128).contiguous(),
+                      y[:, (hq + hkv) * 128:].reshape(1, B, hkv, 128).contiguous(),
+                      kv_va, tok_pos, geo, layer_begin=l)
+
+    def graph_ms(fn):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return best
+
+    t_f = graph_ms(fused) / layers * 1e-3
+    t_u = graph_ms(unfused) / layers * 1e-3
+    nbytes = feats * hidden * 2 + B * hidden * 2 + B * feats * 2
+    try:
+        pk = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+        hbm = pk["hbm_gbs"]
+    except Exception:
+        hbm = 6549.1
+    dev.wait()
+    return {"workload": "Llama-3-8B decode: 64 new tokens, x[64,4096] . W_qkv[6144,4096]^T per layer, "
+                        "K/V into the vTensor cache at token_count",
+            "us_per_layer": round(t_f * 1e6, 2), "GBps": round(nbytes / t_f / 1e9, 1),
+            "frac_of_hbm": round(nbytes / t_f / 1e9 / hbm, 4), "bytes_per_layer": nbytes,
+            "unfused_us_per_layer": round(t_u * 1e6, 2),
+            "speedup_vs_unfused": round(t_u / t_f, 3),
+            "unfused": "cuBLAS GEMM (torch) + vt_kv_append",
+            "kernel": "vt::qkv::qkv_append_kernel<64> (tcgen05/TMA, split-K 2)"}
 
 
 # --------------------------------------------------------- CPU / reference --

@@ -300,7 +300,11 @@ extern "C" int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void*
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
+    // Measured (Llama-3-8B, T=64): ks 1/2/3 = 18.2/16.0/16.9 us — past two
+    // slices the extra reduction outweighs the added SMs (the stream itself
+    // is ~8 us; launch, pipeline fill and the reduction chain are the rest).
     ks = n_sm / (mtiles * ttiles);
+    if (ks > 2) ks = 2;
   }
   ks = ks < 1 ? 1 : (ks > 8 ? 8 : ks);
   if (ks > kblocks) ks = kblocks;
