@@ -110,6 +110,22 @@ int vt_unmap_page(vt_device* dev, int64_t base, int64_t page, int64_t* handle_id
 int vt_release(vt_device* dev, int64_t base);
 int vt_destroy_chunk(vt_device* dev, int64_t handle_id);
 
+/* Cross-device chunk sharing (extends the rTree hard
+ * link of kvsim/scheduler.py:128-130 across pools — no reference counterpart).
+ * vt_export_chunk: a POSIX file descriptor for a live chunk of a CUDA device
+ *   (cuMemExportToShareableHandle); blocks until the chunk exists. The caller
+ *   owns the fd (send it to another process with SCM_RIGHTS, or import it).
+ * vt_import_chunk: takes ownership of fd (closed after the import) and
+ *   returns a new handle ordinal of this device naming the same physical
+ *   memory (cuMemImportFromShareableHandle). It maps like a local chunk — on
+ *   another GPU the mapping's cuMemSetAccess grants this device peer access
+ *   over NVLink — but it is not counted in created_bytes / the budget, and
+ *   neither the import nor its destroy (= dropping this reference) enters the
+ *   call log. Simulated devices return VT_E_ARG. */
+int vt_export_chunk(vt_device* dev, int64_t handle_id, int* fd_out);
+int vt_import_chunk(vt_device* dev, int fd, int64_t* handle_id_out);
+int vt_chunk_is_imported(const vt_device* dev, int64_t handle_id);
+
 /* Batched forms used by VTO map_chunks / _unmap_tail (ops.py:133-146,171-178):
  * identical call-log entries to the per-page loop; stop at the first error and
  * report how many pages were processed in *n_done. */

@@ -21,6 +21,7 @@
 
 #include <cuda.h>
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -31,6 +32,7 @@
 #include <deque>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -71,6 +73,10 @@ struct Driver {
   CUresult (*EventSynchronize)(CUevent);
   CUresult (*EventDestroy)(CUevent);
   CUresult (*GetErrorString)(CUresult, const char**);
+  // Optional (cross-device chunk sharing): nullptr if the driver lacks them.
+  CUresult (*ExportShareable)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                              unsigned long long);
+  CUresult (*ImportShareable)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
   CUresult (*TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave,
@@ -118,6 +124,10 @@ Driver& driver() {
     VT_SYM(GetErrorString, "cuGetErrorString");
     VT_SYM(TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
 #undef VT_SYM
+    d.ExportShareable = reinterpret_cast<decltype(d.ExportShareable)>(
+        dlsym(h, "cuMemExportToShareableHandle"));
+    d.ImportShareable = reinterpret_cast<decltype(d.ImportShareable)>(
+        dlsym(h, "cuMemImportFromShareableHandle"));
     if (ok && d.Init(0) != CUDA_SUCCESS) {
       ok = false;
       d.error += "cuInit failed; ";
@@ -136,7 +146,7 @@ std::string cu_err(CUresult r) {
 // ---------------------------------------------------------------------------
 // Worker-side driver ops.
 // ---------------------------------------------------------------------------
-enum class DrvKind : uint8_t { kCreate, kMap, kUnmap, kDestroy, kRelease };
+enum class DrvKind : uint8_t { kCreate, kMap, kUnmap, kDestroy, kRelease, kExport, kImport };
 
 struct DrvOp {
   DrvKind kind;
@@ -146,6 +156,8 @@ struct DrvOp {
   uint64_t fence_epoch;  // teardown ops wait for this stream event
   uint64_t ticket;
   int64_t submit_ns;
+  int fd;                // import: the shareable handle (consumed)
+  int* fd_out;           // export: where the new shareable handle goes
 };
 
 constexpr int kFenceRing = 64;
@@ -168,6 +180,7 @@ struct vt_device {
   // --- bookkeeping state machine (device.py:127-137) ---
   std::map<int64_t, RangeState> ranges;               // ordered: live_ranges() sorted
   std::map<int64_t, int64_t> handles;                 // id -> map_count, ordered
+  std::set<int64_t> imported;                         // ids of chunks owned by another device
   int64_t next_base = 0;
   int64_t next_handle = 0;
   int64_t mapped_pages = 0;
@@ -201,13 +214,15 @@ struct vt_device {
 
   void note_latency(const DrvOp& op, int64_t done_ns) {
     static const int kOp[] = {VT_OP_CREATE_CHUNK, VT_OP_MAP_PAGE, VT_OP_UNMAP_PAGE,
-                              VT_OP_DESTROY_CHUNK, VT_OP_RELEASE_ADDRESS};
+                              VT_OP_DESTROY_CHUNK, VT_OP_RELEASE_ADDRESS, VT_OP_CREATE_CHUNK,
+                              VT_OP_CREATE_CHUNK};
     std::lock_guard<std::mutex> lk(lat_mu);
     auto& v = lat[kOp[static_cast<int>(op.kind)]];
     if (v.size() < (1u << 20)) v.push_back(done_ns - op.submit_ns);
   }
+  // Imported chunks live in another device's pool and budget.
   int64_t created_bytes() const {
-    return static_cast<int64_t>(handles.size()) * cfg.chunk_bytes;
+    return static_cast<int64_t>(handles.size() - imported.size()) * cfg.chunk_bytes;
   }
   int64_t activation_bytes() const {
     return active_requests * cfg.activation_bytes_per_request;
@@ -365,6 +380,31 @@ struct vt_device {
           ++i;
           break;
         }
+        case DrvKind::kExport: {
+          auto it = phys.find(op.handle_id);
+          if (it == phys.end()) {
+            record_error("export of a chunk the driver never created (id " +
+                         std::to_string(op.handle_id) + ")");
+          } else {
+            CUresult r = d.ExportShareable(op.fd_out, it->second,
+                                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+            if (r != CUDA_SUCCESS) record_error("cuMemExportToShareableHandle: " + cu_err(r));
+          }
+          ++i;
+          break;
+        }
+        case DrvKind::kImport: {
+          CUmemGenericAllocationHandle h = 0;
+          CUresult r = d.ImportShareable(&h, reinterpret_cast<void*>(static_cast<intptr_t>(op.fd)),
+                                         CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+          if (r != CUDA_SUCCESS)
+            record_error("cuMemImportFromShareableHandle: " + cu_err(r));
+          else
+            phys[op.handle_id] = h;
+          ::close(op.fd);
+          ++i;
+          break;
+        }
       }
     }
     const int64_t done = now_ns();
@@ -489,6 +529,9 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
     d->prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     d->prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     d->prop.location.id = cuda_ordinal;
+    // Every chunk can be exported (POSIX fd) so another device's manager can
+    // map it by identity (cross-GPU prefix sharing, vt_export_chunk).
+    if (drv.ExportShareable) d->prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     size_t gran = 0;
     r = drv.Granularity(&gran, &d->prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM);
     if (r != CUDA_SUCCESS || gran == 0 || cfg->chunk_bytes % static_cast<int64_t>(gran) != 0) {
@@ -667,7 +710,9 @@ int vt_destroy_chunk(vt_device* d, int64_t id) {
     return d->fail(VT_E_CHUNK_STILL_MAPPED, "handle " + std::to_string(id) + " still mapped " +
                                                 std::to_string(it->second) + " times");
   d->handles.erase(it);
-  d->log_call(VT_OP_DESTROY_CHUNK, 0, 0, id, 0);
+  // An imported chunk's release drops this device's reference only; it is not
+  // one of the reference's device ops, so it stays out of the call log.
+  if (d->imported.erase(id) == 0) d->log_call(VT_OP_DESTROY_CHUNK, 0, 0, id, 0);
   if (d->is_cuda()) {
     DrvOp op{};
     op.kind = DrvKind::kDestroy;
@@ -676,6 +721,46 @@ int vt_destroy_chunk(vt_device* d, int64_t id) {
     d->kick();
   }
   return VT_OK;
+}
+
+int vt_export_chunk(vt_device* d, int64_t id, int* fd_out) {
+  if (!d->is_cuda()) return d->fail(VT_E_ARG, "a simulated device has no shareable chunks");
+  if (!driver().ExportShareable) return d->fail(VT_E_CUDA, "driver lacks cuMemExportToShareableHandle");
+  if (d->handles.find(id) == d->handles.end())
+    return d->fail(VT_E_STALE_HANDLE,
+                   "handle " + std::to_string(id) + " was destroyed or never created");
+  *fd_out = -1;
+  DrvOp op{};
+  op.kind = DrvKind::kExport;
+  op.handle_id = id;
+  op.fd_out = fd_out;
+  d->enqueue(op);
+  d->kick();
+  const int rc = vt_wait(d, vt_ticket(d));  // the fd is needed now
+  if (rc) return rc;
+  return *fd_out >= 0 ? VT_OK : d->fail(VT_E_CUDA, "export produced no handle");
+}
+
+int vt_import_chunk(vt_device* d, int fd, int64_t* id_out) {
+  if (!d->is_cuda()) return d->fail(VT_E_ARG, "a simulated device cannot import chunks");
+  if (!driver().ImportShareable)
+    return d->fail(VT_E_CUDA, "driver lacks cuMemImportFromShareableHandle");
+  if (fd < 0) return d->fail(VT_E_ARG, "invalid shareable handle");
+  const int64_t h = d->next_handle++;
+  d->handles.emplace(h, 0);
+  d->imported.insert(h);
+  DrvOp op{};
+  op.kind = DrvKind::kImport;
+  op.handle_id = h;
+  op.fd = fd;
+  d->enqueue(op);
+  d->kick();
+  *id_out = h;
+  return VT_OK;
+}
+
+int vt_chunk_is_imported(const vt_device* d, int64_t id) {
+  return d->imported.count(id) ? 1 : 0;
 }
 
 // device.py:166-174

@@ -96,6 +96,10 @@ class PhysicalHandle:
 
     id: int
     map_count: int = 0
+    # True for a chunk imported from another device's pool (export_chunk /
+    # import_chunk): it maps like a local chunk but is never reused for this
+    # pool's own allocations.
+    imported: bool = False
 
 
 @dataclasses.dataclass(frozen=True)
@@ -377,7 +381,27 @@ class VirtualMemoryDevice:
         if rc:
             self._raise(rc)
         self._interned.pop(handle.id, None)
-        self._log_len += 1
+        if not handle.imported:  # dropping an imported reference is not logged
+            self._log_len += 1
+
+    # -- cross-device sharing (include/vtensor.h vt_export_chunk) -------------
+
+    def export_chunk(self, handle: PhysicalHandle) -> int:
+        """POSIX fd naming this chunk's physical memory (caller owns it)."""
+        fd = ctypes.c_int(-1)
+        rc = self._lib.vt_export_chunk(self._h, handle.id, ctypes.byref(fd))
+        if rc:
+            self._raise(rc)
+        return fd.value
+
+    def import_chunk(self, fd: int) -> PhysicalHandle:
+        """Map-able handle of another device's chunk; consumes ``fd``."""
+        rc = self._lib.vt_import_chunk(self._h, int(fd), ctypes.byref(self._i64))
+        if rc:
+            self._raise(rc)
+        handle = PhysicalHandle(id=self._i64.value, imported=True)
+        self._interned[handle.id] = handle
+        return handle
 
     # -- inspection (device.py:272-295) ---------------------------------------
 
