@@ -112,6 +112,8 @@ int vt_destroy_chunk(vt_device* dev, int64_t handle_id);
 
 /* Cross-device chunk sharing (extends the rTree hard
  * link of kvsim/scheduler.py:128-130 across pools — no reference counterpart).
+ * vt_dev_set_shareable: opt in (off by default: shareable allocations cost
+ *   more per cuMemCreate) — chunks created afterwards can be exported.
  * vt_export_chunk: a POSIX file descriptor for a live chunk of a CUDA device
  *   (cuMemExportToShareableHandle); blocks until the chunk exists. The caller
  *   owns the fd (send it to another process with SCM_RIGHTS, or import it).
@@ -122,6 +124,7 @@ int vt_destroy_chunk(vt_device* dev, int64_t handle_id);
  *   over NVLink — but it is not counted in created_bytes / the budget, and
  *   neither the import nor its destroy (= dropping this reference) enters the
  *   call log. Simulated devices return VT_E_ARG. */
+int vt_dev_set_shareable(vt_device* dev, int enabled); /* chunks created afterwards are exportable */
 int vt_export_chunk(vt_device* dev, int64_t handle_id, int* fd_out);
 int vt_import_chunk(vt_device* dev, int fd, int64_t* handle_id_out);
 int vt_chunk_is_imported(const vt_device* dev, int64_t handle_id);

@@ -122,6 +122,7 @@ def vtensor_lib() -> ctypes.CDLL:
         "vt_unmap_page": (c_int, [c_void_p, c_int64, c_int64, P64]),
         "vt_release": (c_int, [c_void_p, c_int64]),
         "vt_destroy_chunk": (c_int, [c_void_p, c_int64]),
+        "vt_dev_set_shareable": (c_int, [c_void_p, c_int]),
         "vt_export_chunk": (c_int, [c_void_p, c_int64, POINTER(c_int)]),
         "vt_import_chunk": (c_int, [c_void_p, c_int, P64]),
         "vt_chunk_is_imported": (c_int, [c_void_p, c_int64]),
@@ -166,5 +167,5 @@ VTENSOR_SYMBOLS = (
     "vt_live_handles", "vt_live_ranges", "vt_range_mappings",
     "vt_call_log_len", "vt_call_log_read", "vt_ticket", "vt_wait", "vt_poll",
     "vt_fence", "vt_set_async", "vt_driver_stats_get", "vt_driver_latencies", "vt_va",
-    "vt_encode_tensor_map", "vt_export_chunk", "vt_import_chunk", "vt_chunk_is_imported",
+    "vt_encode_tensor_map", "vt_dev_set_shareable", "vt_export_chunk", "vt_import_chunk", "vt_chunk_is_imported",
 )

@@ -529,9 +529,6 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
     d->prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     d->prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     d->prop.location.id = cuda_ordinal;
-    // Every chunk can be exported (POSIX fd) so another device's manager can
-    // map it by identity (cross-GPU prefix sharing, vt_export_chunk).
-    if (drv.ExportShareable) d->prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     size_t gran = 0;
     r = drv.Granularity(&gran, &d->prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM);
     if (r != CUDA_SUCCESS || gran == 0 || cfg->chunk_bytes % static_cast<int64_t>(gran) != 0) {
@@ -720,6 +717,20 @@ int vt_destroy_chunk(vt_device* d, int64_t id) {
     d->enqueue(op);
     d->kick();
   }
+  return VT_OK;
+}
+
+int vt_dev_set_shareable(vt_device* d, int enabled) {
+  if (!d->is_cuda()) return enabled ? d->fail(VT_E_ARG, "a simulated device has no shareable chunks")
+                                    : VT_OK;
+  if (enabled && !driver().ExportShareable)
+    return d->fail(VT_E_CUDA, "driver lacks cuMemExportToShareableHandle");
+  // Applies to chunks created from now on (the worker reads prop when it
+  // executes a create; ops already queued keep the old setting only if they
+  // ran before this call, so drain first).
+  vt_wait(d, vt_ticket(d));
+  d->prop.requestedHandleTypes =
+      enabled ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR : CU_MEM_HANDLE_TYPE_NONE;
   return VT_OK;
 }
 

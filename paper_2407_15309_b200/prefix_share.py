@@ -13,6 +13,10 @@ GPU the mapping's cuMemSetAccess grants peer access over NVLink 5, so the
 prefill kernel reads the shared prefix in place through the borrower's VA;
 nothing is copied.
 
+A donor pool opts in with ``device.set_shareable(True)`` before it creates
+the chunks it may share (shareable allocations cost more per cuMemCreate, so
+it is off by default).
+
 Lifetime: the CUDA allocation lives until every device has released its
 handle, so a donor may evict its record while borrowers still read it.
 Imported chunks are outside the borrower's budget (created_bytes) and are

@@ -386,6 +386,12 @@ class VirtualMemoryDevice:
 
     # -- cross-device sharing (include/vtensor.h vt_export_chunk) -------------
 
+    def set_shareable(self, enabled: bool = True) -> None:
+        """Chunks created from now on can be exported (a donor pool opts in)."""
+        rc = self._lib.vt_dev_set_shareable(self._h, int(bool(enabled)))
+        if rc:
+            self._raise(rc)
+
     def export_chunk(self, handle: PhysicalHandle) -> int:
         """POSIX fd naming this chunk's physical memory (caller owns it)."""
         fd = ctypes.c_int(-1)

@@ -29,6 +29,7 @@ PREFIX, NEW = 1024, 256
 
 def _donor(seed=0):
     st = cuda_stack(32, 8, 32, 4096, capacity_chunks=512)
+    st.dev.set_shareable(True)
     base = [(i * 13 + 1) % 501 for i in range(PREFIX)]
     st.sched.create("conv", base)
     st.sched.mark_prefilled("conv")
