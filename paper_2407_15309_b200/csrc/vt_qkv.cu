@@ -61,6 +61,15 @@ struct Args {
   int* counters;              // [mtiles] arrival counters (zero between launches)
 };
 
+// griddepcontrol (PTX 7.8+, sm_90+): no-ops when the launch has no
+// programmatic dependency.
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) { tc::ld16(taddr, r); }
 
 template <int NT>
@@ -98,6 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
+  grid_launch_dependents();  // the next launch may start its own prologue
 
   int it = 0;  // ring position
   {
@@ -105,12 +115,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         const uint64_t once = l2_evict_first_policy();  // W is read once per token tile
         const uint64_t keep = l2_evict_last_policy();   // x is re-read by every feature tile
+        // Programmatic dependent launch: the weights do not depend on the
+        // previous kernel, so the first ring's worth of W streams in while
+        // that kernel drains; x (its output in a real layer stack) is read
+        // only after griddepcontrol.wait.
+        const int pre = min(kb1 - kb0, C::kStages);
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+          tc::tma_load_2d(ring + i * C::kStageBytes, &w_map, &full[i], (kb0 + i) * BK, mtile * BM,
+                          once);
+        }
+        grid_dependency_wait();
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int st = it % C::kStages;
-          if (it >= C::kStages) mbar_wait(&empty[st], ((it / C::kStages) & 1) ^ 1);
           uint8_t* sw = ring + st * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[st], C::kStageBytes);
-          tc::tma_load_2d(sw, &w_map, &full[st], kb * BK, mtile * BM, once);
+          if (it >= pre) {
+            mbar_wait(&empty[st], ((it / C::kStages) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[st], C::kStageBytes);
+            tc::tma_load_2d(sw, &w_map, &full[st], kb * BK, mtile * BM, once);
+          }
           tc::tma_load_2d(sw + BM * BK * 2, &x_map, &full[st], kb * BK, tt * NT, keep);
         }
       }
@@ -148,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // own accumulator, resets the counter, transposes the bf16 tile through
     // shared memory and stores 16-byte vectors (16 lanes per 256-byte row).
     if (warp >= 2) {
+      grid_dependency_wait();  // token tables, q_out and the cache belong to the previous kernel until now
       const int quarter = warp & 3;
       const int row = quarter * 32 + lane;  // this thread's output feature within the tile
       const int ep = threadIdx.x - 64;      // 0..127
@@ -246,8 +270,17 @@ int launch(const CUtensorMap& wm, const CUtensorMap& xm, const Args& a, int mtil
     attr = true;
   }
   const int ttiles = (a.n_tokens + NT - 1) / NT;
-  qkv_append_kernel<NT><<<dim3(mtiles, a.ks, ttiles), kThreads, smem, stream>>>(wm, xm, a);
-  return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(mtiles, a.ks, ttiles);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qkv_append_kernel<NT>, wm, xm, a);
 }
 
 // Split-K workspace: grown on demand, counters zeroed once (the kernel resets
