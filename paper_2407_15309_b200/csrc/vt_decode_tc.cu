@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = sm.tmem_base;
+  tc::grid_launch_dependents();  // the next layer's CTAs may take SMs this grid frees
 
   if (warp == 0) {
     // -------------------------------- producer --------------------------------
@@ -183,12 +184,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&q_map);
       const uint64_t once = l2_evict_first_policy();
       int kc = 0, vc = 0, qc = 0;
+      bool dep_waited = false;
+      auto issue_kv = [&](const CUtensorMap* kvmap, int blk_k, int blk_v, int tok0) {
+        const int c1 = tok0 % a.tpc;
+        const int c3 = tok0 / a.tpc;
+        const int ks = kc % KSTAGES;
+        if (kc >= KSTAGES) mbar_wait(&sm.k_empty[ks], ((kc / KSTAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.k_full[ks], 2 * TILE * 64 * 2);
+        tma_load_4d(sm.k[ks][0], kvmap, &sm.k_full[ks], 0, c1, blk_k, c3, once);
+        tma_load_4d(sm.k[ks][1], kvmap, &sm.k_full[ks], 64, c1, blk_k, c3, once);
+        ++kc;
+        const int vs = vc % VSTAGES;
+        if (vc >= VSTAGES) mbar_wait(&sm.v_empty[vs], ((vc / VSTAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.v_full[vs], 2 * TILE * 64 * 2);
+        tma_load_4d(sm.v[vs][0], kvmap, &sm.v_full[vs], 0, c1, blk_v, c3, once);
+        tma_load_4d(sm.v[vs][1], kvmap, &sm.v_full[vs], 64, c1, blk_v, c3, once);
+        ++vc;
+      };
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         Unit w;
         if (!unit_of(a, sm.lens, u, w)) continue;
         const CUtensorMap* kvmap = a.kv + w.b;
         if (u + static_cast<int>(gridDim.x) < n_units)  // warm the next unit's descriptor
           tma_prefetch_desc(a.kv + ((u + gridDim.x) % (a.batch * a.hkv)) / a.hkv);
+        const int blk_k = (a.layer * 2 + 0) * a.hkv + w.h;
+        const int blk_v = (a.layer * 2 + 1) * a.hkv + w.h;
+        int tok0 = w.t0;
+        if (!dep_waited) {
+          // Programmatic dependent launch: this layer's K/V do not depend on
+          // the previous kernel (in a layer stack, q does), so the first
+          // ring's worth of K/V streams while that kernel drains.
+          for (int j = 0; j < KSTAGES && j < VSTAGES && tok0 < w.t1; ++j, tok0 += TILE)
+            issue_kv(kvmap, blk_k, blk_v, tok0);
+          tc::grid_dependency_wait();
+          dep_waited = true;
+        }
         const int qb = qc & 1;
         if (qc >= 2) mbar_wait(&sm.q_empty[qb], ((qc >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.q_full[qb], 2 * NQ * 64 * 2);
@@ -196,24 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tma_load_2d(sm.q[qb][0], &q_map, &sm.q_full[qb], 0, qrow, once);
         tc::tma_load_2d(sm.q[qb][1], &q_map, &sm.q_full[qb], 64, qrow, once);
         ++qc;
-        const int blk_k = (a.layer * 2 + 0) * a.hkv + w.h;
-        const int blk_v = (a.layer * 2 + 1) * a.hkv + w.h;
-        for (int tok0 = w.t0; tok0 < w.t1; tok0 += TILE) {
-          const int c1 = tok0 % a.tpc;
-          const int c3 = tok0 / a.tpc;
-          const int ks = kc % KSTAGES;
-          if (kc >= KSTAGES) mbar_wait(&sm.k_empty[ks], ((kc / KSTAGES) & 1) ^ 1);
-          mbar_arrive_expect_tx(&sm.k_full[ks], 2 * TILE * 64 * 2);
-          tma_load_4d(sm.k[ks][0], kvmap, &sm.k_full[ks], 0, c1, blk_k, c3, once);
-          tma_load_4d(sm.k[ks][1], kvmap, &sm.k_full[ks], 64, c1, blk_k, c3, once);
-          ++kc;
-          const int vs = vc % VSTAGES;
-          if (vc >= VSTAGES) mbar_wait(&sm.v_empty[vs], ((vc / VSTAGES) & 1) ^ 1);
-          mbar_arrive_expect_tx(&sm.v_full[vs], 2 * TILE * 64 * 2);
-          tma_load_4d(sm.v[vs][0], kvmap, &sm.v_full[vs], 0, c1, blk_v, c3, once);
-          tma_load_4d(sm.v[vs][1], kvmap, &sm.v_full[vs], 64, c1, blk_v, c3, once);
-          ++vc;
-        }
+        for (; tok0 < w.t1; tok0 += TILE) issue_kv(kvmap, blk_k, blk_v, tok0);
       }
     }
     __syncwarp();
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // -------------------------------- epilogue --------------------------------
     // Global writes, the split-arrival atomic and the log-sum-exp merge of a
     // request's splits happen here, off the softmax critical path.
+    tc::grid_dependency_wait();  // outputs and the split workspace: previous kernel's until now
     int uc = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       Unit w;
@@ -351,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const float sl2 = a.scale_log2;
     const int tid = threadIdx.x - 64;  // 0..127
+    tc::grid_dependency_wait();  // (zero outputs of empty requests below)
     int g = 0;
     int uc = 0;  // units handed to the epilogue warp
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -513,6 +528,12 @@ int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
+    // Launched without programmatic dependent launch on purpose: with PDL the
+    // 32 layer launches of a step run back to back with no kernel boundary,
+    // and the driver's concurrent cuMemMap / cuMemSetAccess (the worker's
+    // extends) then slowed from ~0.8 ms to 7.5 ms and surfaced as host waits
+    // (measured: 6077 -> 3968 GB/s per step). The griddepcontrol instructions
+    // in the kernel are no-ops without it.
     kernel<<<grid, kThreads, smem, stream>>>(qmap, a);
   };
   switch (G) {

@@ -61,15 +61,6 @@ struct Args {
   int* counters;              // [mtiles] arrival counters (zero between launches)
 };
 
-// griddepcontrol (PTX 7.8+, sm_90+): no-ops when the launch has no
-// programmatic dependency.
-__device__ __forceinline__ void grid_dependency_wait() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-__device__ __forceinline__ void grid_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) { tc::ld16(taddr, r); }
 
 template <int NT>
@@ -107,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  grid_launch_dependents();  // the next launch may start its own prologue
+  tc::grid_launch_dependents();  // the next launch may start its own prologue
 
   int it = 0;  // ring position
   {
@@ -125,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tma_load_2d(ring + i * C::kStageBytes, &w_map, &full[i], (kb0 + i) * BK, mtile * BM,
                           once);
         }
-        grid_dependency_wait();
+        tc::grid_dependency_wait();
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int st = it % C::kStages;
           uint8_t* sw = ring + st * C::kStageBytes;
@@ -171,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // own accumulator, resets the counter, transposes the bf16 tile through
     // shared memory and stores 16-byte vectors (16 lanes per 256-byte row).
     if (warp >= 2) {
-      grid_dependency_wait();  // token tables, q_out and the cache belong to the previous kernel until now
+      tc::grid_dependency_wait();  // token tables, q_out and the cache belong to the previous kernel until now
       const int quarter = warp & 3;
       const int row = quarter * 32 + lane;  // this thread's output feature within the tile
       const int ep = threadIdx.x - 64;      // 0..127

@@ -69,6 +69,15 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
                : "memory");
 }
 
+// Programmatic dependent launch (griddepcontrol, sm_90+): no-ops when the
+// launch carries no programmatic dependency.
+__device__ __forceinline__ void grid_dependency_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // One lane of a converged warp (elect.sync): warp-uniform operands stay in
 // uniform registers, and only the elected lane issues the tcgen05 op.
 __device__ __forceinline__ bool elect_one() {
