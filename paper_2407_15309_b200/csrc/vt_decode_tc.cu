@@ -326,32 +326,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
-          // Log-sum-exp merge; loads are independent so they overlap (MLP).
+          // Log-sum-exp merge of the request's splits, all G heads at once:
+          // lane l owns head l % G for the (split, head) pairs p = l, l+32, ...
+          // (G divides 32), so each phase is one round of independent loads
+          // plus a shuffle reduction — not G rounds of dependent ones (the
+          // per-head loop made the epilogue warp the bottleneck at G = 8).
           const int64_t u0 = bh * a.n_splits;
           const int S = w.splits_b;
+          const float* ml = a.part_ml + u0 * G * 2;  // [split][head][m, l]
+          float mloc = -INFINITY;
+          for (int p = lane; p < S * G; p += 32) mloc = fmaxf(mloc, __ldcg(ml + p * 2));
+#pragma unroll
+          for (int m = 16; m >= G; m >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, m));
+          float dloc = 0.f;
+          for (int p = lane; p < S * G; p += 32)
+            dloc += tc::ex2(__ldcg(ml + p * 2) - mloc) * __ldcg(ml + p * 2 + 1);
+#pragma unroll
+          for (int m = 16; m >= G; m >>= 1) dloc += __shfl_xor_sync(0xffffffffu, dloc, m);
+          const float inv = dloc > 0.f ? 1.f / dloc : 0.f;
+          float mx_c[G], inv_c[G], acc[G][D / 32];
+#pragma unroll
           for (int c = 0; c < G; ++c) {
-            const float* pm = a.part_ml + (u0 * G + c) * 2;  // stride G*2 per split
-            float mloc = -INFINITY;
-            for (int k = lane; k < S; k += 32) mloc = fmaxf(mloc, __ldcg(pm + k * G * 2));
-            const float mx = warp_max(mloc);
-            float dloc = 0.f;
-            for (int k = lane; k < S; k += 32)
-              dloc += tc::ex2(__ldcg(pm + k * G * 2) - mx) * __ldcg(pm + k * G * 2 + 1);
-            const float den = warp_sum(dloc);
-            float acc[D / 32];
+            mx_c[c] = __shfl_sync(0xffffffffu, mloc, c);
+            inv_c[c] = __shfl_sync(0xffffffffu, inv, c);
 #pragma unroll
-            for (int j = 0; j < D / 32; ++j) acc[j] = 0.f;
-#pragma unroll 4
-            for (int k = 0; k < S; ++k) {
-              const float wgt = tc::ex2(__ldcg(pm + k * G * 2) - mx);
-              const float* po = a.part_o + ((u0 + k) * G + c) * D + lane;
-#pragma unroll
-              for (int j = 0; j < D / 32; ++j) acc[j] = fmaf(wgt, __ldcg(po + 32 * j), acc[j]);
-            }
-            const float inv = den > 0.f ? 1.f / den : 0.f;
-#pragma unroll
-            for (int j = 0; j < D / 32; ++j) dst[c * D + lane + 32 * j] = __float2bfloat16(acc[j] * inv);
+            for (int j = 0; j < D / 32; ++j) acc[c][j] = 0.f;
           }
+          for (int k = 0; k < S; ++k) {
+            const float* po = a.part_o + (u0 + k) * G * D + lane;
+#pragma unroll
+            for (int c = 0; c < G; ++c) {
+              const float wgt = tc::ex2(__ldcg(ml + (k * G + c) * 2) - mx_c[c]);
+#pragma unroll
+              for (int j = 0; j < D / 32; ++j)
+                acc[c][j] = fmaf(wgt, __ldcg(po + c * D + 32 * j), acc[c][j]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < G; ++c)
+#pragma unroll
+            for (int j = 0; j < D / 32; ++j)
+              dst[c * D + lane + 32 * j] = __float2bfloat16(acc[c][j] * inv_c[c]);
         }
       }
       __syncwarp();
