@@ -139,7 +139,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ dist plumbing --
+_COLL_DEVICE = "cuda"
+
+
 def dist_setup(args):
+    """One process per GPU (torchrun). NCCL carries only the barrier and the
+    max/sum of the timings. When more ranks than GPUs are launched (checking
+    the N-rank mechanics on a 1-GPU box) ranks share devices round-robin and
+    the timing reductions go over gloo, since NCCL refuses two ranks on one
+    GPU; numbers from such a run are not scaling numbers."""
+    global _COLL_DEVICE
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -148,11 +157,17 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        n_dev = torch.cuda.device_count()
+        dev = local % n_dev
+        torch.cuda.set_device(dev)
+        if world <= n_dev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+            _COLL_DEVICE = "cpu"
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
-    return world, rank, local
+    return world, rank, torch.cuda.current_device() if torch.cuda.is_available() else local
 
 
 def barrier(world):
@@ -162,26 +177,23 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(x: float, world: int) -> float:
+def _reduce(x: float, world: int, op_name: str) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([x], dtype=torch.float64, device=_COLL_DEVICE)
+    dist.all_reduce(t, op=getattr(dist.ReduceOp, op_name))
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    return _reduce(x, world, "MAX")
 
 
 def sum_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(x, world, "SUM")
 
 
 # ------------------------------------------------------------- the workload --
@@ -452,26 +464,60 @@ def run_ours(args, world, rank, local):
     value = bytes_all / (elapsed_max * 1e-3) / 1e9
 
     # ---- e2e: host buffers through the public API ----
+    # Serving-loop pipeline: the copy engine moves step i+1's q / new K/V in
+    # (pinned host -> HBM) and step i's attention output out (HBM -> pinned
+    # host) on a side stream while step i's kernels run; device buffers are
+    # double-buffered and every hand-off is an event, so no step reads an
+    # input before its copy lands and no output is overwritten before it has
+    # been read back. The timed region closes after the last read-back.
     e2e = None
     if not args.no_e2e:
         host_q = torch.empty(wl.q.shape, dtype=torch.bfloat16, pin_memory=True).copy_(wl.q)
         host_k = torch.empty(wl.k_new.shape, dtype=torch.bfloat16, pin_memory=True).copy_(wl.k_new)
         host_v = torch.empty(wl.v_new.shape, dtype=torch.bfloat16, pin_memory=True).copy_(wl.v_new)
         host_o = torch.empty(wl.out.shape, dtype=torch.bfloat16, pin_memory=True)
-        dq, dk, dv = torch.empty_like(wl.q), torch.empty_like(wl.k_new), torch.empty_like(wl.v_new)
+        bufs = [(torch.empty_like(wl.q), torch.empty_like(wl.k_new), torch.empty_like(wl.v_new),
+                 torch.empty_like(wl.out)) for _ in range(2)]
+        comp = torch.cuda.current_stream()
+        cs = torch.cuda.Stream()
+        in_ready = [torch.cuda.Event() for _ in range(2)]   # H2D into buffer b landed
+        in_free = [torch.cuda.Event() for _ in range(2)]    # step done reading buffer b
+        out_free = [torch.cuda.Event() for _ in range(2)]   # D2H of buffer b's output done
+
+        def h2d(b):
+            dq, dk, dv, _ = bufs[b]
+            with torch.cuda.stream(cs):
+                dq.copy_(host_q, non_blocking=True)
+                dk.copy_(host_k, non_blocking=True)
+                dv.copy_(host_v, non_blocking=True)
+                in_ready[b].record(cs)
+
         e_bytes = 0
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
+        e0.record(comp)
+        cs.wait_event(e0)
+        h2d(0)
+        for i in range(args.steps):
+            b = i & 1
             e_bytes += wl.algorithmic_bytes_per_step()
-            dq.copy_(host_q, non_blocking=True)
-            dk.copy_(host_k, non_blocking=True)
-            dv.copy_(host_v, non_blocking=True)
-            wl.step(q=dq, k_new=dk, v_new=dv)
-            host_o.copy_(wl.out, non_blocking=True)
-        e1.record()
+            if i + 1 < args.steps:
+                if i >= 1:
+                    cs.wait_event(in_free[b ^ 1])  # step i-1 has finished reading it
+                h2d(b ^ 1)
+            dq, dk, dv, do = bufs[b]
+            comp.wait_event(in_ready[b])
+            if i >= 2:
+                comp.wait_event(out_free[b])       # step i-2's output has been read back
+            wl.step(q=dq, k_new=dk, v_new=dv, out=do)
+            in_free[b].record(comp)
+            cs.wait_event(in_free[b])
+            with torch.cuda.stream(cs):
+                host_o.copy_(do, non_blocking=True)
+                out_free[b].record(cs)
+        comp.wait_stream(cs)
+        e1.record(comp)
         torch.cuda.synchronize()
         e_ms = max_over_ranks(e0.elapsed_time(e1), world)
         e_all = sum_over_ranks(e_bytes, world)
@@ -479,7 +525,8 @@ def run_ours(args, world, rank, local):
                "tokens_per_s": round(wl.B * args.steps * world / (e_ms * 1e-3), 1),
                "ms_per_step": round(e_ms / args.steps, 4),
                "h2d_bytes_per_step": int((host_q.numel() + host_k.numel() + host_v.numel()) * 2),
-               "d2h_bytes_per_step": int(host_o.numel() * 2)}
+               "d2h_bytes_per_step": int(host_o.numel() * 2),
+               "pipeline": "copies on a side stream overlap the previous/next step (double-buffered)"}
 
     map_lat = sorted(wl.dev.driver_latencies("map_page")) or [0]
     drv_end = wl.dev.driver_stats()
@@ -857,6 +904,11 @@ def run_reference(args, world, rank):
 
 def main():
     args = parse()
+    hang_s = float(os.environ.get("VT_BENCH_HANG_DUMP_S", "0"))
+    if hang_s > 0:  # diagnostics: dump every thread's stack if the run wedges
+        import faulthandler
+
+        faulthandler.dump_traceback_later(hang_s, exit=True)
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))

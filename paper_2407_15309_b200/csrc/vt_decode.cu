@@ -430,6 +430,7 @@ extern "C" size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t bat
                                             int32_t max_seq_len, int32_t split_tokens) {
   // sized for the smallest split either path may pick (tc_split >= 128 tokens per
   // split only when it needs <= 16 splits; CUDA-core default >= 512)
+  if (max_seq_len < 1) max_seq_len = 1;  // all-empty batches still get a valid size
   const int split = split_tokens > 0 ? split_tokens : std::min(default_split(max_seq_len, false),
                                                                (max_seq_len + 15) / 16);
   const int64_t n_splits = (max_seq_len + split - 1) / split;
@@ -468,7 +469,10 @@ static int decode_impl(const vt_kv_geometry* g, int32_t layer, const void* q,
                     : tc             ? tc_split(batch, g->kv_heads, max_seq_len, num_sms())
                                      : default_split(max_seq_len, false);
   if (split % kStageTok) return cudaErrorInvalidValue;
-  if (batch <= 0 || max_seq_len <= 0) return 0;
+  if (batch <= 0) return 0;
+  if (max_seq_len <= 0)  // every request is empty: softmax over nothing is defined as zeros
+    return cudaMemsetAsync(out, 0, static_cast<size_t>(batch) * g->q_heads * kD * 2,
+                           static_cast<cudaStream_t>(stream));
   const int n_splits = (max_seq_len + split - 1) / split;
   if (workspace_bytes < vt_decode_workspace_bytes(g, batch, max_seq_len, split))
     return cudaErrorInvalidValue;

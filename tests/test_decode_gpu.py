@@ -25,6 +25,7 @@ CASES = {
     "llama8b_gqa4": (32, 8, 32, 4352, [0, 1, 15, 16, 17, 100, 1000, 4096]),
     "llama70b_shard_gqa8": (16, 2, 16, 4096, [5, 128, 129, 2049, 4096]),
     "gqa2": (4, 4, 8, 2048, [33, 1024, 2000]),
+    "all_empty": (32, 8, 32, 4352, [0, 0, 0]),  # max_seq_len 0: zeros, no split math
 }
 
 
@@ -49,7 +50,7 @@ def test_decode_matches_oracle(cuda_ok, name, path, split):
     out = decode_attention(q, kv_va, seq, layer, st.geo, max(lens), split_tokens=split,
                            kv_maps=maps)
     torch.cuda.synchronize()
-    assert last_launches() >= 1
+    assert last_launches() >= (1 if max(lens) else 0)  # all-empty: a memset, no kernel
     ks, vs = gather(st, kv_va, lens, layer)
     ref = decode_attention_ref(q.cpu(), ks, vs)
     err = rel_err(out.cpu(), ref)
