@@ -93,20 +93,31 @@ int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                          const void* kv_maps, const int32_t* start, int32_t batch,
                          int32_t n_new, float scale, void* out, void* stream);
 
-/* Fused QKV projection + KV append, tcgen05/TMA with
- * split-K (fp32 partials in a library-owned workspace, last slice reduces):
+/* Fused QKV projection + KV append, tcgen05; each
+ * 128-feature tile's K halves run on a 2-CTA cluster and are reduced through
+ * distributed shared memory (no global workspace):
  *   qkv = x . W^T    x [n_tokens, hidden] bf16, W [(Hq+2Hkv)*head_dim, hidden]
- *                    bf16 (nn.Linear layout), fp32 accumulate
+ *                    bf16 (nn.Linear layout) passed PACKED (vt_qkv_pack_weight),
+ *                    fp32 accumulate
  * Q rows -> q_out [n_tokens, q_heads, head_dim] bf16; K and V rows are written
  * straight into request tok_req[t]'s VA (kv_va[tok_req[t]]) at token position
  * tok_pos[t] of `layer`, in the vt_kv_append layout (the page must be mapped:
  * the manager's extend ticket was waited on, kvsim/scheduler.py:189-205).
- * hidden % 64 == 0. split_k <= 0 picks the K split that fills the SMs.
+ * hidden % 64 == 0. split_k: CTAs per feature tile, 1 or 2 (0 = auto: 2
+ * unless the tile grid alone fills the SMs twice over); > 2 is an error.
  *   tok_req, tok_pos : [n_tokens] i32 (device);  kv_va : [n_req] u64 (device) */
-int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x, const void* w,
+int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x, const void* w_packed,
                   int32_t hidden, int32_t n_tokens, const int32_t* tok_req,
                   const int32_t* tok_pos, const uint64_t* kv_va, void* q_out, int32_t split_k,
                   void* stream);
+
+/* Rewrite a QKV weight W [feats, hidden] bf16 (row-major) once into the
+ * streaming layout vt_qkv_append reads: [feats/128][hidden/64] blocks of
+ * 128 x 64 bf16 (16 KiB, SWIZZLE_128B K-major), so each CTA's share of the
+ * weight is one contiguous byte range. Same size as W; feats % 128 == 0,
+ * hidden % 64 == 0, 16-byte aligned pointers. Stream-ordered. */
+int vt_qkv_pack_weight(const void* w, int32_t feats, int32_t hidden, void* w_packed,
+                       void* stream);
 
 /* Number of kernel launches the last call on this thread issued (bench
  * accounting of "gpu_launches"). */

@@ -56,6 +56,8 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_qkv_append.argtypes = [POINTER(_Geo), c_int32, P, P, c_int32, c_int32, P, P, P, P,
                                       c_int32, P]
         lib.vt_qkv_append.restype = c_int
+        lib.vt_qkv_pack_weight.argtypes = [P, c_int32, c_int32, P, P]
+        lib.vt_qkv_pack_weight.restype = c_int
         lib.vt_attn_last_launches.argtypes = []
         lib.vt_attn_last_launches.restype = c_int32
         _lib = lib
@@ -65,6 +67,7 @@ def attn_lib() -> ctypes.CDLL:
 ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_paged",
                 "vt_decode_workspace_bytes", "vt_kv_append",
                 "vt_kv_tensor_maps", "vt_prefill_attention", "vt_qkv_append",
+                "vt_qkv_pack_weight",
                 "vt_attn_last_launches")
 
 
@@ -172,27 +175,57 @@ def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, kv_va: torch.Tensor,
     _check(rc, "vt_kv_append")
 
 
-def qkv_append(x: torch.Tensor, w_qkv: torch.Tensor, tok_req: torch.Tensor,
+class PackedQKVWeight:
+    """A QKV weight rewritten once into the streaming layout of the fused
+    kernel (include/vt_attention.h vt_qkv_pack_weight): 128 x 64 blocks of 16
+    KiB, [feature tile][k block], pre-swizzled for the MMA. Same byte size as
+    the ``[(Hq + 2 Hkv) * d, hidden]`` nn.Linear weight it came from."""
+
+    def __init__(self, w_qkv: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+        if w_qkv.dtype != torch.bfloat16 or w_qkv.dim() != 2 or not w_qkv.is_contiguous():
+            raise ValueError("w_qkv must be a contiguous bf16 [features, hidden] tensor")
+        _need_cuda(w_qkv)
+        self.shape = tuple(w_qkv.shape)
+        self.data = torch.empty_like(w_qkv)
+        rc = attn_lib().vt_qkv_pack_weight(w_qkv.data_ptr(), self.shape[0], self.shape[1],
+                                           self.data.data_ptr(), _stream(stream))
+        _check(rc, "vt_qkv_pack_weight")
+
+
+def pack_qkv_weight(w_qkv: torch.Tensor,
+                    stream: torch.cuda.Stream | None = None) -> PackedQKVWeight:
+    return PackedQKVWeight(w_qkv, stream)
+
+
+def qkv_append(x: torch.Tensor, w_qkv: "PackedQKVWeight | torch.Tensor", tok_req: torch.Tensor,
                tok_pos: torch.Tensor, kv_va: torch.Tensor, geo: KVGeometry, layer: int,
                q_out: torch.Tensor | None = None, split_k: int = 0,
                stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Fused QKV projection + KV append (include/vt_attention.h vt_qkv_append).
 
-    x ``[T, hidden]`` bf16, w_qkv ``[(Hq + 2 Hkv) * d, hidden]`` bf16. Returns q
-    ``[T, Hq, d]``; K/V of token t land in the cache of request ``tok_req[t]``
-    at position ``tok_pos[t]`` of ``layer`` (its page must already be mapped)."""
+    x ``[T, hidden]`` bf16; w_qkv a :class:`PackedQKVWeight` of the
+    ``[(Hq + 2 Hkv) * d, hidden]`` bf16 weight (a plain tensor is packed on
+    every call — an extra pass over the weight, for one-off use only). Returns
+    q ``[T, Hq, d]``; K/V of token t land in the cache of request
+    ``tok_req[t]`` at position ``tok_pos[t]`` of ``layer`` (its page must
+    already be mapped). ``split_k`` = CTAs per 128-feature tile: 1, or 2
+    (the K halves on a 2-CTA cluster, reduced through distributed shared
+    memory); 0 picks automatically."""
     T, hidden = x.shape
     feats = (geo.q_heads + 2 * geo.kv_heads) * geo.head_dim
-    if x.dtype != torch.bfloat16 or w_qkv.dtype != torch.bfloat16 or tuple(w_qkv.shape) != (feats, hidden):
-        raise ValueError(f"x must be bf16 [T, hidden], w_qkv bf16 [{feats}, hidden]")
-    if not (x.is_contiguous() and w_qkv.is_contiguous()):
-        raise ValueError("x and w_qkv must be contiguous")
+    if isinstance(w_qkv, torch.Tensor):
+        w_qkv = PackedQKVWeight(w_qkv, stream)
+    if x.dtype != torch.bfloat16 or w_qkv.shape != (feats, hidden):
+        raise ValueError(f"x must be bf16 [T, hidden], w_qkv [{feats}, hidden]")
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
     if q_out is None:
         q_out = torch.empty(T, geo.q_heads, geo.head_dim, dtype=torch.bfloat16, device=x.device)
-    _need_cuda(x, w_qkv, tok_req, tok_pos, kv_va, q_out)
-    rc = attn_lib().vt_qkv_append(ctypes.byref(_geo(geo)), layer, x.data_ptr(), w_qkv.data_ptr(),
-                                  hidden, T, tok_req.data_ptr(), tok_pos.data_ptr(),
-                                  kv_va.data_ptr(), q_out.data_ptr(), split_k, _stream(stream))
+    _need_cuda(x, w_qkv.data, tok_req, tok_pos, kv_va, q_out)
+    rc = attn_lib().vt_qkv_append(ctypes.byref(_geo(geo)), layer, x.data_ptr(),
+                                  w_qkv.data.data_ptr(), hidden, T, tok_req.data_ptr(),
+                                  tok_pos.data_ptr(), kv_va.data_ptr(), q_out.data_ptr(), split_k,
+                                  _stream(stream))
     _check(rc, "vt_qkv_append")
     return q_out
 

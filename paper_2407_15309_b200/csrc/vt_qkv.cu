@@ -1,5 +1,5 @@
 // Fused QKV projection + KV append into the vTensor cache (SURVEY.md §8(f)
-// row 2) — tcgen05 + TMEM + TMA, split-K with an arrival-counter reduction, sm_100a.
+// row 2) — tcgen05 + TMEM, K split across a 2-CTA cluster, sm_100a.
 //
 //   qkv[t, f] = sum_k x[t, k] * W[f, k]          (bf16 in, fp32 accumulate)
 //   f <  Hq*d           -> q_out[t, f]                         (bf16)
@@ -10,22 +10,36 @@
 //                          kvsim/scheduler.py:189-205: the page holding
 //                          tok_pos[t] is mapped before this launch).
 //
-// D^T = W x^T: the weight tile is the M=128 operand (output features), the
-// tokens are N (NT = 64/128/256 per tile), K = hidden in 64-element SW128
-// blocks. Decode (T = batch) streams the 50 MB Llama-3-8B QKV weight once
-// per layer — HBM-bound — so the K dimension is split into KS slices
-// (n_feature_tiles x KS ~ 148 SMs, one wave): each CTA accumulates its slice
-// in TMEM, writes the fp32 partial to an L2-resident workspace and the last
-// slice to arrive reduces and stores (a self-resetting arrival counter per
-// tile). A thread-block-cluster/DSMEM reduction was measured first: clusters
-// of 3 do not all co-schedule on the GPCs (48 x 3 CTAs ran in two waves).
+// D^T = W x^T: a 128-feature weight block is the M=128 operand, the tokens are
+// N (NT = 64/128/256 per tile), K = hidden in 64-element blocks. In decode
+// (T = batch) the layer streams its 50 MB Llama-3-8B weight once — HBM-bound —
+// so the work is laid out for streaming:
 //
-// Grid: (feature tile, K slice, token tile); one output tile per CTA.
+// * Packed weight. vt_qkv_pack_weight rewrites W once (weights are static)
+//   into [feature tile][k block] blocks of 128 x 64 bf16 = 16 KiB, each already
+//   in the SWIZZLE_128B K-major layout the MMA descriptor reads, so a CTA's
+//   share of the weight is ONE contiguous byte range pulled with 16 KiB bulk
+//   copies (no tensor map, sequential DRAM pages).
+// * K split over a CTA pair (thread-block cluster of 2). Each feature tile is
+//   computed by two CTAs, one per half of `hidden`; the upper CTA stages its
+//   fp32 partial in its own (by then idle) ring and ONE bulk copy moves it
+//   into the lower CTA's ring over distributed shared memory, completing on
+//   the lower CTA's mbarrier; the lower CTA adds it and stores. The reduction
+//   never touches global memory. Measured alternatives (tools/trace_qkv.py
+//   timelines): a global split-K reduction (fp32 partials in L2 + arrival
+//   counter) with a stream-K split over every SM streamed the weight at
+//   6.9 TB/s but its chain of L2 round trips (~1 us each under load) added a
+//   5-6 us tail; per-thread DSMEM stores of the partial took 1.4 us (scalar,
+//   coalesced) / 2.3 us (16-byte, strided) against 0.8 us for the bulk copy.
+//   Clusters of 2 all co-schedule (74 at one CTA per SM; clusters of 3 do
+//   not: 45 < 48 tiles).
 //
-// Warp roles (192 threads): warp 0 TMA producer (W and x tiles, 192 KiB
-// ring: 8 stages at NT=64), warp 1 MMA issuer (one elected lane), warps 2-5
-// epilogue (thread = TMEM lane = output feature; 16-byte row stores after a
-// transpose through shared memory).
+// Warp roles (192 threads): warp 0 producer (packed W + x tiles, 192 KiB
+// ring), warp 1 MMA issuer (one elected lane), warps 2-5 epilogue (thread =
+// TMEM lane = output feature). Stores go through a per-warp staging tile as
+// 16-byte vectors; the destination rows (for K/V one per request, in as many
+// different 2 MiB pages) are tabulated and prefetched into L2 while the
+// weight streams, so their address translation is off the critical path.
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -39,51 +53,105 @@ namespace vt {
 namespace qkv {
 
 constexpr int BM = 128;  // output features per tile
-constexpr int BK = 64;   // hidden elements per k-block (one 128-byte SW128 row)
+constexpr int BK = 64;   // hidden elements per k block (one 128-byte SW128 row)
+constexpr int kBlockBytes = BM * BK * 2;  // one packed weight block (16 KiB)
 constexpr int kThreads = 192;
 constexpr int kRingBytes = 192 * 1024;
 
 template <int NT>
 struct Cfg {
-  static constexpr int kStageBytes = BM * BK * 2 + NT * BK * 2;
+  static constexpr int kXBytes = NT * BK * 2;
+  static constexpr int kStageBytes = kBlockBytes + kXBytes;
   static constexpr int kStages = kRingBytes / kStageBytes;
+  static constexpr int kTmemCols = NT;
   static_assert(kStages >= 2, "ring too small");
+  static_assert(NT * BM * 4 <= kRingBytes, "the peer partial must fit the ring");
 };
 
 struct Args {
+  const uint8_t* w_packed;    // [mtiles][kblocks][16 KiB]
   __nv_bfloat16* q_out;       // [T, Hq, d]
   const uint64_t* kv_va;      // [n_req]
   const int32_t* tok_req;     // [T]
   const int32_t* tok_pos;     // [T]
-  int32_t n_tokens, hidden, hq, hkv, tpc, layer, ks, kblocks;
+  int32_t n_tokens, hq, hkv, tpc, layer, kblocks;
   int64_t chunk_bytes;
-  float* ws;                  // [mtiles][ks][NT][BM] fp32 split-K partials
-  int* counters;              // [mtiles] arrival counters (zero between launches)
 };
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) { tc::ld16(taddr, r); }
+// ------------------------------------------------- cluster / DSMEM helpers --
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// Address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// Bulk copy of `bytes` from this CTA's shared memory into a peer CTA's,
+// completing on the peer's mbarrier (SASS UBLKCP over DSMEM).
+__device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                            uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst_cluster), "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void arrive_peer(uint32_t bar_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_addr)
+               : "memory");
+}
+#ifdef VT_QKV_TRACE
+// Debug timeline (tools/gpu_trace_qkv.sh): per CTA, %globaltimer at
+// 0 entry, 1 setup done, 2 first W copy issued, 3 first stage landed,
+// 4 last stage landed, 5 last MMA committed, 6 accumulator ready,
+// 7 peer handshake done, 8 partial received / sent, 9 epilogue done.
+__device__ long long g_qkv_trace[512][10];
+__device__ __forceinline__ void trace(int i) {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.y == 0 && blockIdx.x < 512) g_qkv_trace[blockIdx.x][i] = t;
+}
+#define QKV_TRACE(i) trace(i)
+#else
+#define QKV_TRACE(i)
+#endif
 
-template <int NT>
+// KS = CTAs per feature tile (1, or 2 = cluster pair). Grid: (mtiles * KS, token tiles).
+template <int NT, int KS>
 __global__ void __launch_bounds__(kThreads, 1)
-    qkv_append_kernel(const __grid_constant__ CUtensorMap w_map,
-                      const __grid_constant__ CUtensorMap x_map, const Args a) {
+    qkv_append_kernel(const __grid_constant__ CUtensorMap x_map, const Args a) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   __shared__ uint64_t full[C::kStages], empty[C::kStages], acc_full;
-  __shared__ uint64_t row_dst[NT];  // destination of each token's 256-byte head row
-  __shared__ int last_flag;
+  __shared__ uint64_t peer_ready;    // (upper CTA) the lower CTA's ring is free
+  __shared__ uint64_t partial_full;  // (lower CTA) the upper CTA's partial has landed
+  __shared__ uint64_t row_dst[NT];   // destination of each token's 256-byte head row
+  __shared__ __align__(16) __nv_bfloat16 stage_out[4][16][32];  // per epilogue warp
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int mtile = blockIdx.x;
-  const int slice = blockIdx.y;  // K slice of this CTA
-  const int kb0 = slice * a.kblocks / a.ks;
-  const int kb1 = (slice + 1) * a.kblocks / a.ks;
-  const int tt = blockIdx.z;  // token tile
-  const int tile_id = mtile * gridDim.z + tt;  // split-K reduction group
+  const int m = blockIdx.x / KS;                       // feature tile
+  const uint32_t half = KS == 2 ? cluster_rank() : 0;  // K half of this CTA
+  const int tt = blockIdx.y;                           // token tile
+  const int KB = a.kblocks;
+  const int mid = KS == 2 ? KB / 2 : KB;  // (finishing the lower half earlier was measured: no gain)
+  const int kb0 = half == 0 ? 0 : mid;
+  const int kb1 = half == 0 ? mid : KB;
+  if (threadIdx.x == 0) QKV_TRACE(0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::kStages; ++i) {
@@ -91,213 +159,234 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[i], 1);
     }
     mbar_init(&acc_full, 1);
+    mbar_init(&peer_ready, 1);
+    mbar_init(&partial_full, 1);  // the lower CTA's expect_tx; the bulk copy completes it
     fence_mbar_init();
   }
-  if (warp == 1) tc::alloc(&tmem_base, NT);
+  if (warp == 1) tc::alloc(&tmem_base, C::kTmemCols);
   tc::fence_before();
-  __syncthreads();
+  if constexpr (KS == 2) {
+    cluster_sync();  // the peer's barriers are initialised before any remote arrive
+  } else {
+    __syncthreads();
+  }
   tc::fence_after();
   const uint32_t tmem = tmem_base;
   tc::grid_launch_dependents();  // the next launch may start its own prologue
+  if (threadIdx.x == 0) QKV_TRACE(1);
 
-  int it = 0;  // ring position
-  {
-    if (warp == 0) {
-      if (lane == 0) {
-        const uint64_t once = l2_evict_first_policy();  // W is read once per token tile
-        const uint64_t keep = l2_evict_last_policy();   // x is re-read by every feature tile
-        // Programmatic dependent launch: the weights do not depend on the
-        // previous kernel, so the first ring's worth of W streams in while
-        // that kernel drains; x (its output in a real layer stack) is read
-        // only after griddepcontrol.wait.
-        const int pre = min(kb1 - kb0, C::kStages);
-        for (int i = 0; i < pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], C::kStageBytes);
-          tc::tma_load_2d(ring + i * C::kStageBytes, &w_map, &full[i], (kb0 + i) * BK, mtile * BM,
-                          once);
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t once = l2_evict_first_policy();  // W is read once per token tile
+      const uint64_t keep = l2_evict_last_policy();   // x is re-read by every feature tile
+      const int n = kb1 - kb0;
+      const uint64_t wsrc = reinterpret_cast<uint64_t>(a.w_packed) +
+                            (static_cast<uint64_t>(m) * KB + kb0) * kBlockBytes;
+      // Programmatic dependent launch: the weights do not depend on the
+      // previous kernel, so the first ring's worth streams in while that
+      // kernel drains; x (its output in a real layer stack) only after
+      // griddepcontrol.wait.
+      const int pre = min(n, C::kStages);
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+        bulk_g2s(ring + i * C::kStageBytes, wsrc + static_cast<uint64_t>(i) * kBlockBytes,
+                 kBlockBytes, &full[i], once);
+        if (i == 0) QKV_TRACE(2);
+      }
+      tc::grid_dependency_wait();
+      for (int i = 0; i < n; ++i) {
+        const int st = i % C::kStages;
+        uint8_t* sw = ring + st * C::kStageBytes;
+        if (i >= pre) {
+          mbar_wait(&empty[st], ((i / C::kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], C::kStageBytes);
+          bulk_g2s(sw, wsrc + static_cast<uint64_t>(i) * kBlockBytes, kBlockBytes, &full[st], once);
         }
-        tc::grid_dependency_wait();
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int st = it % C::kStages;
-          uint8_t* sw = ring + st * C::kStageBytes;
-          if (it >= pre) {
-            mbar_wait(&empty[st], ((it / C::kStages) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[st], C::kStageBytes);
-            tc::tma_load_2d(sw, &w_map, &full[st], kb * BK, mtile * BM, once);
-          }
-          tc::tma_load_2d(sw + BM * BK * 2, &x_map, &full[st], kb * BK, tt * NT, keep);
+        tc::tma_load_2d(sw + kBlockBytes, &x_map, &full[st], (kb0 + i) * BK, tt * NT, keep);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    constexpr uint32_t id = tc::idesc_bf16(BM, NT, false, false);
+    constexpr uint32_t hi = tc::sdesc_hi(1024);
+    for (int i = 0; i < kb1 - kb0; ++i) {
+      const int st = i % C::kStages;
+      mbar_wait(&full[st], (i / C::kStages) & 1);
+      tc::fence_after();
+#ifdef VT_QKV_TRACE
+      if (lane == 0 && i == 0) QKV_TRACE(3);
+      if (lane == 0 && i == kb1 - kb0 - 1) QKV_TRACE(4);
+#endif
+      const uint32_t base = smem_u32(ring + st * C::kStageBytes);
+      const uint32_t la = tc::sdesc_lo(base, 16);
+      const uint32_t lb = tc::sdesc_lo(base + kBlockBytes, 16);
+      if (tc::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          tc::mma_ss(tmem, la + 2 * kk, hi, lb + 2 * kk, hi, id, (i > 0 || kk > 0) ? 1u : 0u);
+        tc::commit(&empty[st]);
+        if (i == kb1 - kb0 - 1) {
+          tc::commit(&acc_full);
+          QKV_TRACE(5);
         }
       }
       __syncwarp();
-    } else if (warp == 1) {
-      constexpr uint32_t id = tc::idesc_bf16(BM, NT, false, false);
-      constexpr uint32_t hi = tc::sdesc_hi(1024);
-      for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        const int st = it % C::kStages;
-        mbar_wait(&full[st], (it / C::kStages) & 1);
-        tc::fence_after();
-        const uint32_t base = smem_u32(ring + st * C::kStageBytes);
-        const uint32_t la = tc::sdesc_lo(base, 16);
-        const uint32_t lb = tc::sdesc_lo(base + BM * BK * 2, 16);
-        if (tc::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            tc::mma_ss(tmem, la + 2 * kk, hi, lb + 2 * kk, hi, id, (kb > kb0 || kk > 0) ? 1u : 0u);
-          tc::commit(&empty[st]);
-          if (kb == kb1 - 1) tc::commit(&acc_full);
+    }
+  } else {
+    // ------------------------------ epilogue ---------------------------------
+    // A feature tile is exactly one head of q, K or V (feature boundaries are
+    // multiples of 128), so for every token its 128 outputs form one
+    // contiguous 256-byte row at the destination.
+    tc::grid_dependency_wait();  // token tables, q_out and the cache belong to the previous kernel until now
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // this thread's output feature within the tile
+    const int ep = threadIdx.x - 64;      // 0..127
+    float* peer_part = reinterpret_cast<float*>(ring);  // [NT][BM] fp32 partial (both CTAs)
+    if (half == 0) {
+      const int kind = m < a.hq ? 0 : (m < a.hq + a.hkv ? 1 : 2);  // q | K | V
+      const int head = kind == 0 ? m : (kind == 1 ? m - a.hq : m - a.hq - a.hkv);
+      for (int i = ep; i < NT; i += 128) {
+        const int t = tt * NT + i;
+        uint64_t dst = 0;
+        if (t < a.n_tokens) {
+          if (kind == 0) {
+            dst = reinterpret_cast<uint64_t>(a.q_out) + (static_cast<uint64_t>(t) * a.hq + head) * 256;
+          } else {
+            const int pos = a.tok_pos[t];
+            const int chunk = pos / a.tpc;
+            dst = a.kv_va[a.tok_req[t]] + static_cast<uint64_t>(chunk) * a.chunk_bytes +
+                  (static_cast<uint64_t>(a.layer * 2 + kind - 1) * a.hkv + head) * a.tpc * 256 +
+                  static_cast<uint64_t>(pos - chunk * a.tpc) * 256;
+          }
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(dst));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(dst + 128));
         }
-        __syncwarp();
+        row_dst[i] = dst;
+      }
+      named_bar_sync(1, 128);
+    }
+    mbar_wait(&acc_full, 0);
+    tc::fence_after();
+    if (ep == 0) QKV_TRACE(6);
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    if (KS == 2 && half == 1) {
+      // upper half: stage the fp32 partial [NT][BM] in our own ring (free:
+      // our MMAs are done), then one bulk copy into the lower CTA's ring once
+      // its MMAs are done too, completing on its barrier
+#pragma unroll 1
+      for (int c = 0; c < NT; c += 32) {
+        uint32_t r0[16], r1[16];
+        tc::ld16(lane_addr + c, r0);
+        tc::ld16(lane_addr + c + 16, r1);
+        tc::wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          peer_part[(c + i) * BM + row] = __uint_as_float(r0[i]);
+          peer_part[(c + 16 + i) * BM + row] = __uint_as_float(r1[i]);
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> the bulk copy's reads
+      named_bar_sync(1, 128);
+      if (ep == 0) {
+        mbar_wait(&peer_ready, 0);
+        QKV_TRACE(7);
+        bulk_s2peer(peer_addr(peer_part, 0), peer_part, NT * BM * 4, peer_addr(&partial_full, 0));
+        bulk_wait_read();  // our shared memory must outlive the copy's reads
+        QKV_TRACE(8);
       }
     } else {
-      it += kb1 - kb0;
-    }
-
-    // ------------------------------ epilogue ---------------------------------
-    // The feature tile is exactly one head of q, K or V (feature boundaries
-    // are multiples of 128), so for every token its 128 outputs form one
-    // contiguous 256-byte row at the destination. While the MMAs run, the
-    // epilogue warps tabulate those row addresses. Split-K: every K slice
-    // writes its fp32 partial tile to the workspace and bumps the tile's
-    // arrival counter; the slice that arrives last sums the others into its
-    // own accumulator, resets the counter, transposes the bf16 tile through
-    // shared memory and stores 16-byte vectors (16 lanes per 256-byte row).
-    if (warp >= 2) {
-      tc::grid_dependency_wait();  // token tables, q_out and the cache belong to the previous kernel until now
-      const int quarter = warp & 3;
-      const int row = quarter * 32 + lane;  // this thread's output feature within the tile
-      const int ep = threadIdx.x - 64;      // 0..127
-      {
-        const int hq = a.hq, hkv = a.hkv;
-        const int kind = mtile < hq ? 0 : (mtile < hq + hkv ? 1 : 2);  // q | K | V
-        const int head = kind == 0 ? mtile : (kind == 1 ? mtile - hq : mtile - hq - hkv);
-        for (int i = ep; i < NT; i += 128) {
-          const int t = tt * NT + i;
-          uint64_t dst = 0;
-          if (t < a.n_tokens) {
-            if (kind == 0) {
-              dst = reinterpret_cast<uint64_t>(a.q_out) + (static_cast<uint64_t>(t) * hq + head) * 256;
-            } else {
-              const int pos = a.tok_pos[t];
-              const int chunk = pos / a.tpc;
-              dst = a.kv_va[a.tok_req[t]] + static_cast<uint64_t>(chunk) * a.chunk_bytes +
-                    (static_cast<uint64_t>(a.layer * 2 + kind - 1) * hkv + head) * a.tpc * 256 +
-                    static_cast<uint64_t>(pos - chunk * a.tpc) * 256;
-            }
-          }
-          row_dst[i] = dst;
-        }
-      }
-      mbar_wait(&acc_full, 0);
-      tc::fence_after();
-      const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      bool last = true;
-      if (a.ks > 1) {
-        // partial [NT][BM] fp32 (coalesced across the warp's 32 features)
-        float* mine = a.ws + (static_cast<size_t>(tile_id) * a.ks + slice) * NT * BM;
-#pragma unroll 1
-        for (int c = 0; c < NT; c += 16) {
-          uint32_t r[16];
-          tmem_ld16(lane_addr + c, r);
-          tc::wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) __stcg(mine + (c + i) * BM + row, __uint_as_float(r[i]));
-        }
-        __threadfence();
-        named_bar_sync(1, 128);
+      if (KS == 2) {
         if (ep == 0) {
-          const int old = atomicAdd(a.counters + tile_id, 1);
-          last_flag = old == a.ks - 1;
-          if (last_flag) a.counters[tile_id] = 0;  // self-resetting for the next launch
+          mbar_arrive_expect_tx(&partial_full, NT * BM * 4);
+          arrive_peer(peer_addr(&peer_ready, 1));  // our ring is free
         }
-        named_bar_sync(1, 128);
-        last = last_flag;
-        if (last) __threadfence();
+        mbar_wait(&partial_full, 0);
+        if (ep == 0) QKV_TRACE(8);
       }
-      if (last) {
-        __nv_bfloat16* tile_t = reinterpret_cast<__nv_bfloat16*>(ring);  // [NT][BM] bf16
 #pragma unroll 1
-        for (int c = 0; c < NT; c += 16) {
-          uint32_t r[16];
-          tmem_ld16(lane_addr + c, r);
-          tc::wait_ld();
-          float v[16];
+      for (int c = 0; c < NT; c += 32) {
+        uint32_t r0[16], r1[16];
+        tc::ld16(lane_addr + c, r0);
+        tc::ld16(lane_addr + c + 16, r1);
+        tc::wait_ld();
+        float v[32];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-          for (int p = 0; p < a.ks; ++p) {
-            if (p == slice) continue;
-            const float* src = a.ws + (static_cast<size_t>(tile_id) * a.ks + p) * NT * BM;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += __ldcg(src + (c + i) * BM + row);
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) tile_t[(c + i) * BM + row] = __float2bfloat16_rn(v[i]);
+        for (int i = 0; i < 16; ++i) {
+          v[i] = __uint_as_float(r0[i]);
+          v[16 + i] = __uint_as_float(r1[i]);
         }
-        named_bar_sync(1, 128);
-        const int sub = ep & 15;
-#pragma unroll 4
-        for (int i = ep >> 4; i < NT; i += 8) {
-          const uint64_t dst = row_dst[i];
-          if (dst)
-            *reinterpret_cast<uint4*>(dst + sub * 16) =
-                *reinterpret_cast<const uint4*>(tile_t + i * BM + sub * 8);
+        if (KS == 2) {  // lower half + upper half: a fixed order, bit-reproducible
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += peer_part[(c + i) * BM + row];
+        }
+        // transpose through this warp's staging tile (16 tokens x 32
+        // features), then 16-byte stores (4 per 64-byte token row segment)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            stage_out[quarter][i][lane] = __float2bfloat16_rn(v[h * 16 + i]);
+          __syncwarp();
+#pragma unroll
+          for (int j = lane; j < 64; j += 32) {
+            const uint64_t dst = row_dst[c + h * 16 + (j >> 2)];
+            if (dst)
+              *reinterpret_cast<uint4*>(dst + quarter * 64 + (j & 3) * 16) =
+                  *reinterpret_cast<const uint4*>(&stage_out[quarter][j >> 2][(j & 3) * 8]);
+          }
+          __syncwarp();
         }
       }
     }
+    if (ep == 0) QKV_TRACE(9);
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (warp == 1) tc::dealloc(tmem, NT);
+  if (warp == 1) tc::dealloc(tmem, C::kTmemCols);
 }
 
-template <int NT>
-int launch(const CUtensorMap& wm, const CUtensorMap& xm, const Args& a, int mtiles,
-           cudaStream_t stream) {
+// W [feats, hidden] row-major -> [feats/128][hidden/64][128 x 64] blocks in the
+// SWIZZLE_128B K-major layout (16-byte chunk c of row r stored at c ^ (r & 7)).
+// One thread per 16-byte chunk of the output (coalesced stores).
+__global__ void pack_weight_kernel(const uint4* __restrict__ w, int hidden, long long n_chunks,
+                                   uint4* __restrict__ out) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n_chunks) return;
+  const int kblocks = hidden / BK;
+  const long long blk = idx >> 10;  // 1024 chunks per 16 KiB block
+  const int within = static_cast<int>(idx & 1023);
+  const int r = within >> 3;
+  const int c = (within & 7) ^ (r & 7);
+  const long long m = blk / kblocks;
+  const int kb = static_cast<int>(blk - m * kblocks);
+  out[idx] = w[((m * BM + r) * hidden + kb * BK + c * 8) >> 3];
+}
+
+template <int NT, int KS>
+int launch(const CUtensorMap& xm, const Args& a, int mtiles, int ttiles, cudaStream_t stream) {
   const size_t smem = kRingBytes + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(qkv_append_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(qkv_append_kernel<NT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
-  const int ttiles = (a.n_tokens + NT - 1) / NT;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(mtiles, a.ks, ttiles);
+  cfg.gridDim = dim3(mtiles * KS, ttiles, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = KS;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, qkv_append_kernel<NT>, wm, xm, a);
-}
-
-// Split-K workspace: grown on demand, counters zeroed once (the kernel resets
-// each counter after use). One per process; calls are stream-ordered.
-struct Workspace {
-  float* partials = nullptr;
-  size_t partial_bytes = 0;
-  int* counters = nullptr;
-  int n_counters = 0;
-};
-int workspace(size_t partial_bytes, int n_counters, Workspace** out) {
-  static Workspace w;
-  if (partial_bytes > w.partial_bytes) {
-    if (w.partials) cudaFree(w.partials);
-    if (cudaMalloc(&w.partials, partial_bytes) != cudaSuccess) return cudaErrorMemoryAllocation;
-    w.partial_bytes = partial_bytes;
-  }
-  if (n_counters > w.n_counters) {
-    if (w.counters) cudaFree(w.counters);
-    if (cudaMalloc(&w.counters, n_counters * sizeof(int)) != cudaSuccess)
-      return cudaErrorMemoryAllocation;
-    cudaMemset(w.counters, 0, n_counters * sizeof(int));
-    w.n_counters = n_counters;
-  }
-  *out = &w;
-  return 0;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, qkv_append_kernel<NT, KS>, xm, a);
 }
 
 }  // namespace qkv
@@ -305,48 +394,44 @@ int workspace(size_t partial_bytes, int n_counters, Workspace** out) {
 
 using namespace vt::qkv;
 
-extern "C" int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x, const void* w,
-                             int32_t hidden, int32_t n_tokens, const int32_t* tok_req,
-                             const int32_t* tok_pos, const uint64_t* kv_va, void* q_out,
-                             int32_t split_k, void* stream) {
+#ifdef VT_QKV_TRACE
+extern "C" int vt_qkv_trace(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_qkv_trace, sizeof(g_qkv_trace));
+}
+#endif
+
+extern "C" int vt_qkv_pack_weight(const void* w, int32_t feats, int32_t hidden, void* w_packed,
+                                  void* stream) {
+  if (feats <= 0 || hidden <= 0 || feats % BM || hidden % BK) return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(w_packed)) & 15)
+    return cudaErrorInvalidValue;
+  const long long n_chunks = static_cast<long long>(feats) * hidden / 8;
+  const int threads = 256;
+  pack_weight_kernel<<<static_cast<unsigned>((n_chunks + threads - 1) / threads), threads, 0,
+                       static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4*>(w), hidden,
+                                                            n_chunks, static_cast<uint4*>(w_packed));
+  return cudaGetLastError();
+}
+
+extern "C" int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x,
+                             const void* w_packed, int32_t hidden, int32_t n_tokens,
+                             const int32_t* tok_req, const int32_t* tok_pos, const uint64_t* kv_va,
+                             void* q_out, int32_t split_k, void* stream) {
   if (g->head_dim != 128 || hidden <= 0 || hidden % BK) return cudaErrorInvalidValue;
+  if (reinterpret_cast<uintptr_t>(w_packed) & 15) return cudaErrorInvalidValue;
+  if (split_k > 2) return cudaErrorInvalidValue;
   if (n_tokens <= 0) return 0;
   const int feats = (g->q_heads + 2 * g->kv_heads) * 128;
   const int mtiles = feats / BM;
   const int kblocks = hidden / BK;
   const int nt = n_tokens <= 64 ? 64 : (n_tokens <= 128 ? 128 : 256);
   const int ttiles = (n_tokens + nt - 1) / nt;
-  int ks = split_k;
-  if (ks <= 0) {  // fill the SMs: feature tiles x token tiles x K slices ~ one wave
-    static int n_sm = 0;
-    if (!n_sm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    // Measured (Llama-3-8B, T=64): ks 1/2/3 = 18.2/16.0/16.9 us — past two
-    // slices the extra reduction outweighs the added SMs (the stream itself
-    // is ~8 us; launch, pipeline fill and the reduction chain are the rest).
-    ks = n_sm / (mtiles * ttiles);
-    if (ks > 2) ks = 2;
-  }
-  ks = ks < 1 ? 1 : (ks > 8 ? 8 : ks);
-  if (ks > kblocks) ks = kblocks;
-  Workspace* wsp = nullptr;
-  if (ks > 1) {
-    const int groups = mtiles * ttiles;
-    int rc = workspace(static_cast<size_t>(groups) * ks * nt * BM * 4, groups, &wsp);
-    if (rc) return rc;
-  }
+  // Two CTAs per feature tile (K halves, cluster pair) unless the caller pins
+  // one, or the tile grid alone already covers the SMs several times over.
+  const int ks = split_k > 0 ? split_k : (kblocks >= 2 && mtiles * ttiles < 296 ? 2 : 1);
+  if (ks == 2 && kblocks < 2) return cudaErrorInvalidValue;
 
-  CUtensorMap wm, xm;
-  {
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(hidden), static_cast<cuuint64_t>(feats)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(hidden) * 2};
-    const cuuint32_t box[2] = {BK, BM};
-    int rc = vt::encode_tensor_map_bf16(&wm, const_cast<void*>(w), 2, dims, strides, box);
-    if (rc) return rc;
-  }
+  CUtensorMap xm;
   {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(hidden), static_cast<cuuint64_t>(n_tokens)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(hidden) * 2};
@@ -355,29 +440,29 @@ extern "C" int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void*
     if (rc) return rc;
   }
   Args a{};
+  a.w_packed = static_cast<const uint8_t*>(w_packed);
   a.q_out = static_cast<__nv_bfloat16*>(q_out);
   a.kv_va = kv_va;
   a.tok_req = tok_req;
   a.tok_pos = tok_pos;
   a.n_tokens = n_tokens;
-  a.hidden = hidden;
   a.hq = g->q_heads;
   a.hkv = g->kv_heads;
   a.tpc = g->tokens_per_chunk;
   a.layer = layer;
-  a.ks = ks;
   a.kblocks = kblocks;
   a.chunk_bytes = g->chunk_bytes;
-  a.ws = wsp ? wsp->partials : nullptr;
-  a.counters = wsp ? wsp->counters : nullptr;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rc;
-  if (nt == 64)
-    rc = launch<64>(wm, xm, a, mtiles, s);
-  else if (nt == 128)
-    rc = launch<128>(wm, xm, a, mtiles, s);
-  else
-    rc = launch<256>(wm, xm, a, mtiles, s);
+  if (ks == 2) {
+    rc = nt == 64    ? launch<64, 2>(xm, a, mtiles, ttiles, s)
+         : nt == 128 ? launch<128, 2>(xm, a, mtiles, ttiles, s)
+                     : launch<256, 2>(xm, a, mtiles, ttiles, s);
+  } else {
+    rc = nt == 64    ? launch<64, 1>(xm, a, mtiles, ttiles, s)
+         : nt == 128 ? launch<128, 1>(xm, a, mtiles, ttiles, s)
+                     : launch<256, 1>(xm, a, mtiles, ttiles, s);
+  }
   if (rc) return rc;
   return cudaGetLastError();
 }

@@ -1,8 +1,11 @@
 """Fused QKV projection + KV append on the B200.
 
-The kernel computes qkv = x · W_qkvᵀ (bf16 in, fp32 accumulate, split-K over a
-thread-block cluster) and writes K/V of token t straight into the vTensor
-cache of request tok_req[t] at tok_pos[t]. Checked against a torch fp32 GEMM
+The kernel computes qkv = x · W_qkvᵀ from the packed weight (bf16 in, fp32
+accumulate; each feature tile's K halves on a 2-CTA cluster, the upper half's
+partial added by the lower CTA through distributed shared memory) and writes
+K/V of token t straight into the vTensor cache of request tok_req[t] at
+tok_pos[t]. Cases cover one and two CTAs per tile, token tiles of 64/128/256
+and several token tiles (more clusters than SMs). Checked against a torch fp32 GEMM
 of the same bf16 inputs (the oracle for a floating-point kernel); tolerance
 2e-2 relative (north_star), measured ~4e-3 (one bf16 rounding). Every other
 KV row of the written layer and every other layer must be byte-identical.
@@ -12,7 +15,7 @@ import pytest
 import torch
 
 from oracle.attention_ref import rel_err
-from paper_2407_15309_b200.attention import decode_attention, qkv_append
+from paper_2407_15309_b200.attention import decode_attention, pack_qkv_weight, qkv_append
 from paper_2407_15309_b200.kv_layout import chunk_view
 from vt_gpu_util import admit_with_lengths, cuda_stack
 
@@ -24,6 +27,9 @@ CASES = {
     "llama8b_decode_b64_nosplit": (32, 8, 32, 4096, list(range(3, 3 + 64 * 17, 17)), 1, 1),
     "prefill_chunks_300_tokens": (32, 8, 32, 4096, [16, 40, 0], 100, 0),
     "gqa8_hidden_1024_split2": (16, 2, 16, 1024, [5, 17, 33, 129], 3, 2),
+    "gqa8_hidden_1024_auto": (16, 2, 16, 1024, [5, 17, 33, 129], 3, 0),
+    "llama8b_b100_nt128": (32, 8, 32, 4096, list(range(7, 7 + 100 * 9, 9)), 1, 0),
+    "prefill_1000_tokens_multi_segment": (32, 8, 32, 4096, [0, 16, 100, 333], 250, 0),
 }
 
 
@@ -49,7 +55,7 @@ def test_qkv_append_matches_torch(cuda_ok, name):
     pages = [st.sched.mem[f"req{i}"].vt.space.mapped_pages for i in range(len(lens))]
     before = [chunk_view(va, p, st.geo).clone() for va, p in zip(kv_va.tolist(), pages)]
 
-    q = qkv_append(x, w, tok_req, tok_pos, kv_va, st.geo, layer, split_k=split_k)
+    q = qkv_append(x, pack_qkv_weight(w), tok_req, tok_pos, kv_va, st.geo, layer, split_k=split_k)
     torch.cuda.synchronize()
 
     ref = (x.float() @ w.float().T).view(T, hq + 2 * hkv, 128)

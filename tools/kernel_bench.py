@@ -197,7 +197,7 @@ def bench_qkv(args, pk):
     Baseline in the same run: cuBLAS GEMM (torch) + vt_kv_append (unfused).
     Both timed as device time from a CUDA graph of 20 calls (4 weights of
     50 MB rotate, so W is never L2-resident)."""
-    from paper_2407_15309_b200.attention import kv_append, qkv_append
+    from paper_2407_15309_b200.attention import kv_append, pack_qkv_weight, qkv_append
     L, hkv, hq, hidden = 32, 8, 32, 4096
     res = []
     for B in args.qkv_batch:
@@ -214,13 +214,14 @@ def bench_qkv(args, pk):
         tok_pos = torch.full((B,), 100, dtype=torch.int32, device="cuda")
         feats = (hq + 2 * hkv) * 128
         ws = [(torch.randn(feats, hidden, device="cuda") / 64).to(torch.bfloat16) for _ in range(4)]
+        packed = [pack_qkv_weight(w) for w in ws]
         x = torch.randn(B, hidden, device="cuda").to(torch.bfloat16)
         q = torch.empty(B, hq, 128, dtype=torch.bfloat16, device="cuda")
         nbytes = feats * hidden * 2 + B * hidden * 2 + B * feats * 2
         lay = [0]
         for split in args.qkv_split:
             def fn():
-                qkv_append(x, ws[lay[0] % 4], tok_req, tok_pos, kv_va, geo, lay[0] % L, q_out=q,
+                qkv_append(x, packed[lay[0] % 4], tok_req, tok_pos, kv_va, geo, lay[0] % L, q_out=q,
                            split_k=split)
                 lay[0] += 1  # 4 weights x 50 MB rotate: never L2-resident
             ms, _ = timed_graph(fn)

@@ -1,0 +1,56 @@
+"""Debug aid: per-CTA timeline of the fused QKV kernel (libvtattn.so built with
+-DVT_QKV_TRACE; tools/gpu_trace_qkv.sh). Llama-3-8B, B tokens, one launch
+after warm-up (cold W: a different weight than the warm-up calls)."""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+sys.path[:0] = [".", "tools"]
+import kernel_bench as kb
+from paper_2407_15309_b200.attention import attn_lib, pack_qkv_weight, qkv_append
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+split = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+L, hkv, hq, hidden = 32, 8, 32, 4096
+cfg, dev, ops, sched, geo = kb.stack(L, hkv, hq, 4096, 4096)
+vas = []
+for b in range(B):
+    sched.create(f"r{b}", [1] * 100)
+    sched.mark_prefilled(f"r{b}")
+    sched.extend(f"r{b}", 101)
+    vas.append(dev.va(sched.mem[f"r{b}"].vt.space.rng))
+dev.wait()
+kv_va = torch.tensor(vas, dtype=torch.int64, device="cuda")
+tok_req = torch.arange(B, dtype=torch.int32, device="cuda")
+tok_pos = torch.full((B,), 100, dtype=torch.int32, device="cuda")
+feats = (hq + 2 * hkv) * 128
+ws = [pack_qkv_weight((torch.randn(feats, hidden, device="cuda") / 64).to(torch.bfloat16)) for _ in range(4)]
+x = torch.randn(B, hidden, device="cuda").to(torch.bfloat16)
+for i in range(3):
+    qkv_append(x, ws[i], tok_req, tok_pos, kv_va, geo, 0, split_k=split)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+qkv_append(x, ws[3], tok_req, tok_pos, kv_va, geo, 0, split_k=split)
+e1.record()
+torch.cuda.synchronize()
+print(f"B={B} split={split} event time {e0.elapsed_time(e1)*1e3:.1f} us")
+buf = (ctypes.c_longlong * (512 * 10))()
+lib = attn_lib()
+lib.vt_qkv_trace(buf)
+a = np.frombuffer(buf, dtype=np.int64).reshape(512, 10)
+a = a[a[:, 0] > 0]
+t0 = a[:, 0].min()
+names = ["entry", "setup", "w_issue", "first_land", "last_land", "last_commit", "acc_ready",
+         "peer_ready", "partial", "end"]
+r = a - t0
+r[a == 0] = -1
+print("ctas", len(a))
+for lab, sel in (("lower", np.arange(len(a)) % 2 == 0), ("upper", np.arange(len(a)) % 2 == 1)):
+    for j, n in enumerate(names):
+        col = r[sel, j]
+        col = col[col >= 0]
+        if len(col):
+            print(f"{lab} {n:12s} min {col.min():7d} p50 {int(np.median(col)):7d} max {col.max():7d} ns")
