@@ -140,14 +140,19 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 }
 
 #ifdef VT_PF_TRACE
-// Debug timeline of CTA (0,0,0) (clock64): [slot][j][0]=S ready, [1]=P arrived;
-// mma[j][s]=group {PV_s(j), S_s(j+1)} issued.
-__device__ long long g_pf_trace_sm[2][64][2];
-__device__ long long g_pf_trace_mma[64][2];
-#define VT_TRACE(cond, dst) \
-  if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) dst = clock64();
+// Debug timeline of CTA 0 (clock64), per global key block g < 256:
+// [0]/[2] slot 0/1 S ready (after s_full), [1]/[3] slot 0/1 P arrived,
+// [4]/[5] MMA group {PV_s(g), S_s(g+1)} issued for slot 0/1,
+// [6]/[7] slot 0 epilogue start / end (at the item's last g).
+__device__ long long g_pf_trace[256][8];
+__device__ long long g_pf_sub[256][4];  // slot 0 row 0: ld done, max done, exp done, st done
+#define VT_SUB(cond, g, k) \
+  if ((cond) && blockIdx.x == 0 && (g) < 256) g_pf_sub[(g)][(k)] = clock64();
+#define VT_TRACE(cond, g, k) \
+  if ((cond) && blockIdx.x == 0 && (g) < 256) g_pf_trace[(g)][(k)] = clock64();
 #else
-#define VT_TRACE(cond, dst)
+#define VT_TRACE(cond, g, k)
+#define VT_SUB(cond, g, k)
 #endif
 
 struct Args {
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (s < nslots) {
               const bool last_slot = s == nslots - 1;
               wait_fence(&sm.p_full[s], g & 1);
+              VT_TRACE(lane == 0, g, 4 + s);
               if (tc::elect_one()) {
                 mma_pv(s, g, j == 0);
                 if (last_slot) tc::commit(&sm.v_empty[g % kStages]);
@@ -352,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kpos0 = j * BN;
           mbar_wait(&sm.s_full[s], g & 1);
           tc::fence_after();
+          VT_TRACE(row == 0, g, 2 * s);
           float x[BN];
           {
             uint32_t r[BN];
@@ -361,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < BN; ++k) x[k] = __uint_as_float(r[k]);
           }
+          VT_SUB(row == 0 && s == 0, g, 0);
           if (kpos0 + BN - 1 > qmin || kpos0 + BN > it.kv_len) {
             const int lim = min(qpos + 1, it.kv_len) - kpos0;  // keys [0, lim) are visible
 #pragma unroll
@@ -379,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                        fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
           }
+          VT_SUB(row == 0 && s == 0 && mx > -1e30f, g, 1);
           const float mx_s = mx * sl2;
           const bool grow = mx_s > m_run + kRescaleLog2;  // false while both are -inf
           const float m_new = grow ? mx_s : m_run;
@@ -404,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
           l_run = fmaf(l_run, alpha, a01.x + a01.y);
           m_run = m_new;
+          VT_SUB(row == 0 && s == 0 && l_run > -1.f, g, 2);
           // P -> TMEM over the first 64 S columns: column c = keys (2c, 2c+1) as bf16x2.
           tmem_st32(s_addr, pr);
           tmem_st32(s_addr + 32, pr + 32);
@@ -441,11 +451,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             zeroed = true;
           }
           tc::wait_st();
+          VT_SUB(row == 0 && s == 0, g, 3);
           if (zeroed) fence_proxy_async_smem();
           tc::fence_before();
           mbar_arrive(&sm.p_full[s]);
+          VT_TRACE(row == 0, g, 2 * s + 1);
         }
         // epilogue: PV(n_kv-2) completed before S(n_kv-1); wait for the last PV.
+        VT_TRACE(row == 0 && s == 0, g - 1, 6);
         mbar_wait(&sm.o_done[s], (g - 1) & 1);
         tc::fence_after();
         const int tok = it.t * BM + row;
@@ -470,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // O is read: the next item's PV(0) (acc = 0) may overwrite it. That
         // PV waits for this warpgroup's next P, which comes after this point.
         tc::fence_before();
+        VT_TRACE(row == 0 && s == 0, g - 1, 7);
       }
     }
   }
@@ -485,9 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 using namespace vt::pf;
 
 #ifdef VT_PF_TRACE
-extern "C" int vt_prefill_trace(long long* out) {  // 2*64*2 + 64*2 values
-  cudaMemcpyFromSymbol(out, g_pf_trace_sm, sizeof(g_pf_trace_sm));
-  return cudaMemcpyFromSymbol(out + 2 * 64 * 2, g_pf_trace_mma, sizeof(g_pf_trace_mma));
+extern "C" int vt_prefill_trace(long long* out) {  // 256 x 8 + 256 x 4 values
+  cudaMemcpyFromSymbol(out + 256 * 8, g_pf_sub, sizeof(g_pf_sub));
+  return cudaMemcpyFromSymbol(out, g_pf_trace, sizeof(g_pf_trace));
 }
 #endif
 
