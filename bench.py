@@ -827,15 +827,19 @@ def cpu_baseline(cfg_name: str, budget_s: float = 8.0) -> dict:
             "host_cpus": os.cpu_count(), "cpu_model": cpu_name}
 
 
-def manager_cpu_baseline() -> dict:
+def manager_cpu_baseline(reference_only: bool = False) -> dict:
     """vTensor extend / append on the host, 1 core: the reference's algorithm
     (oracle/vtm_ref.py, reference cost model) vs this package's manager on the
     simulated shim (same op stream, Llama-3-8B geometry, 64 requests at ~4k)."""
-    import paper_2407_15309_b200 as vt
     from oracle import vtm_ref as R
 
+    arms = [("reference_port", R)]
+    if not reference_only:
+        import paper_2407_15309_b200 as vt
+
+        arms.append(("ours_host_side", vt))
     out = {}
-    for name, ns in (("reference_port", R), ("ours_host_side", vt)):
+    for name, ns in arms:
         cfg = ns.SimConfig(capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB, weights_bytes=0,
                            geometry=ns.ModelGeometry(32, 8, 128, 2), max_seq_len=8192,
                            initial_alloc_tokens=0)
@@ -900,6 +904,9 @@ def run_reference(args, world, rank):
                          "cores": torch.get_num_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        # the metric's other half: vTensor extend / token append through the
+        # reference's manager algorithm (oracle/vtm_ref.py), 1 host core
+        "extend": manager_cpu_baseline(reference_only=True)["reference_port"],
     }
     print(json.dumps(line))
 
