@@ -99,7 +99,8 @@ def timed_graph(fn, reps=20, iters=10):
 
 def bench_decode(args, pk):
     # 8b: Llama-3-8B (G=4, tpc 16); 70b: one 16-layer group of Llama-2-70B (G=8, tpc 32)
-    L, hkv, hq, B, ctx = (32, 8, 32, 64, 4096) if args.shape == "8b" else (16, 8, 64, 64, 4096)
+    L, hkv, hq, B, ctx = {"8b": (32, 8, 32, 64, 4096), "70b": (16, 8, 64, 64, 4096),
+                          "toy": (1, 8, 8, 8, 4096), "mha64": (4, 8, 8, 64, 4096)}[args.shape]
     cfg, dev, ops, sched, geo = stack(L, hkv, hq, ctx + 256, 20000)
     gen = torch.Generator(device="cuda").manual_seed(0)
     vas = []
@@ -253,7 +254,7 @@ def main():
     ap.add_argument("--splits", type=lambda s: [int(x) for x in s.split(",")], default=[1024])
     ap.add_argument("--paths", type=lambda s: s.split(","), default=["tcgen05", "cuda_core"])
     ap.add_argument("--loop", action="store_true", help="time 32 back-to-back launches")
-    ap.add_argument("--shape", choices=["8b", "70b"], default="8b")
+    ap.add_argument("--shape", choices=["8b", "70b", "toy", "mha64"], default="8b")
     ap.add_argument("--qkv-batch", type=lambda s: [int(x) for x in s.split(",")], default=[64])
     ap.add_argument("--qkv-split", type=lambda s: [int(x) for x in s.split(",")], default=[0])
     ap.add_argument("--pf-batch", type=int, default=16, help="prefill: requests (config 3: 16)")
