@@ -3,9 +3,27 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace vt {
+
+// Host: cudaFuncSetAttribute is per device, so remember per kernel which
+// devices already have the dynamic shared-memory limit raised (a process may
+// drive several GPUs, e.g. cross-device prefix sharing).
+template <typename Kernel>
+inline void set_smem_limit_once(Kernel kernel, size_t bytes, std::atomic<uint64_t>& devices) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(devices.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(bytes));
+    devices.fetch_or(bit, std::memory_order_release);
+  }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -377,12 +377,8 @@ __global__ void __launch_bounds__(kD) decode_combine_kernel(const DecodeArgs a, 
 template <int G>
 cudaError_t launch_decode(const DecodeArgs& args, dim3 grid, cudaStream_t stream) {
   const size_t smem = sizeof(DecodeSmem<G>);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(decode_splitkv_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_devices{0};
+  set_smem_limit_once(decode_splitkv_kernel<G>, smem, attr_devices);
   decode_splitkv_kernel<G><<<grid, kThreads, smem, stream>>>(args);
   return cudaGetLastError();
 }

@@ -563,12 +563,8 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   a.n_items = a.n_qtiles * a.pairs * batch;
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t smem = sizeof(Smem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_devices{0};
+  vt::set_smem_limit_once(prefill_kernel, smem, attr_devices);
   static int n_sm = 0;
   if (!n_sm) {
     int dev = 0;

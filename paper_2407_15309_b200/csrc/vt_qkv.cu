@@ -366,12 +366,8 @@ __global__ void pack_weight_kernel(const uint4* __restrict__ w, int hidden, long
 template <int NT, int KS>
 int launch(const CUtensorMap& xm, const Args& a, int mtiles, int ttiles, cudaStream_t stream) {
   const size_t smem = kRingBytes + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(qkv_append_kernel<NT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_devices{0};
+  set_smem_limit_once(qkv_append_kernel<NT, KS>, smem, attr_devices);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(mtiles * KS, ttiles, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
