@@ -51,6 +51,18 @@ int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                         int32_t batch, int32_t max_seq_len, float scale, void* out,
                         void* workspace, size_t workspace_bytes, int32_t split_tokens,
                         void* stream);
+
+/* Same as vt_decode_attention, for a layer launched right after another
+ * decode layer on the same stream (the layers of one step after its KV
+ * append): the tcgen05 kernel then uses programmatic dependent launch, so its
+ * first K/V tiles stream while the previous layer drains. Contract: the K/V
+ * this call reads were written by kernels that completed before the previous
+ * kernel on the stream started. Same arguments and errors. */
+int vt_decode_attention_chained(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                const uint64_t* kv_va, const void* kv_maps,
+                                const int32_t* seq_lens, int32_t batch, int32_t max_seq_len,
+                                float scale, void* out, void* workspace, size_t workspace_bytes,
+                                int32_t split_tokens, void* stream);
 size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t batch, int32_t max_seq_len,
                                  int32_t split_tokens);
 

@@ -174,7 +174,7 @@ class GpuCompute:
         for layer in range(q.shape[0]):
             decode_attention(q[layer], kv_va, seq, layer, self.geo, mx, out=out[layer],
                              workspace=self.ws, split_tokens=self.split, kv_maps=maps,
-                             stream=stream)
+                             stream=stream, chained=layer > 0)
             self.launches += last_launches()
         self.dev.fence(stream.cuda_stream)
         return out

@@ -40,6 +40,8 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_decode_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, P, c_int32, c_int32,
                                             c_float, P, P, c_size_t, c_int32, P]
         lib.vt_decode_attention.restype = c_int
+        lib.vt_decode_attention_chained.argtypes = lib.vt_decode_attention.argtypes
+        lib.vt_decode_attention_chained.restype = c_int
         lib.vt_decode_attention_paged.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, P,
                                                   c_int32, c_int32, c_float, P, P, c_size_t,
                                                   c_int32, P]
@@ -64,7 +66,7 @@ def attn_lib() -> ctypes.CDLL:
     return _lib
 
 
-ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_paged",
+ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_chained", "vt_decode_attention_paged",
                 "vt_decode_workspace_bytes", "vt_kv_append",
                 "vt_kv_tensor_maps", "vt_prefill_attention", "vt_qkv_append",
                 "vt_qkv_pack_weight",
@@ -109,13 +111,15 @@ def decode_attention(q: torch.Tensor, kv_va: torch.Tensor, seq_lens: torch.Tenso
                      geo: KVGeometry, max_seq_len: int, out: torch.Tensor | None = None,
                      workspace: DecodeWorkspace | None = None, scale: float | None = None,
                      split_tokens: int = 0, stream: torch.cuda.Stream | None = None,
-                     kv_maps: torch.Tensor | None = None) -> torch.Tensor:
+                     kv_maps: torch.Tensor | None = None, chained: bool = False) -> torch.Tensor:
     """q ``[B, Hq, d]`` bf16 -> out ``[B, Hq, d]`` bf16 for one layer.
 
     ``kv_va`` is an int64 CUDA tensor of request VAs (``device.va(space.rng)``),
     ``seq_lens`` an int32 CUDA tensor; ``max_seq_len`` a host bound on it.
     With ``kv_maps`` (:class:`KVMapCache`) the tcgen05/TMEM kernel runs;
-    without, the CUDA-core cp.async.bulk kernel."""
+    without, the CUDA-core cp.async.bulk kernel. ``chained=True`` for a layer
+    launched right after another decode layer on the same stream
+    (``vt_decode_attention_chained``: programmatic dependent launch)."""
     B = q.shape[0]
     if q.dtype != torch.bfloat16 or q.shape[1:] != (geo.q_heads, geo.head_dim):
         raise ValueError(f"q must be bf16 [B, {geo.q_heads}, {geo.head_dim}]")
@@ -130,7 +134,8 @@ def decode_attention(q: torch.Tensor, kv_va: torch.Tensor, seq_lens: torch.Tenso
     if kv_maps is not None:
         _need_cuda(kv_maps)
         maps_ptr = kv_maps.data_ptr()
-    rc = attn_lib().vt_decode_attention(
+    fn = attn_lib().vt_decode_attention_chained if chained else attn_lib().vt_decode_attention
+    rc = fn(
         ctypes.byref(_geo(geo)), layer, q.data_ptr(), kv_va.data_ptr(), maps_ptr,
         seq_lens.data_ptr(), B,
         max_seq_len, scale, out.data_ptr(), workspace.buf.data_ptr(), workspace.buf.numel(),

@@ -439,7 +439,8 @@ extern "C" size_t vt_decode_workspace_bytes(const vt_kv_geometry* g, int32_t bat
 int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
                         const void* kv_maps, const int32_t* seq_lens, int32_t batch,
                         int32_t n_splits, int32_t split, float scale, void* out, float* part_o,
-                        float* part_ml, int32_t* arrivals, int32_t n_sms, cudaStream_t stream);
+                        float* part_ml, int32_t* arrivals, int32_t n_sms, bool pdl,
+                        cudaStream_t stream);
 
 static int num_sms() {
   static int n = 0;
@@ -456,7 +457,7 @@ static int decode_impl(const vt_kv_geometry* g, int32_t layer, const void* q,
                        int32_t max_blocks, uint64_t pool_base, const int32_t* seq_lens,
                        int32_t batch, int32_t max_seq_len, float scale, void* out,
                        void* workspace, size_t workspace_bytes, int32_t split_tokens,
-                       void* stream) {
+                       bool chained, void* stream) {
   g_last_launches = 0;
   if (g->head_dim != kD || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
   const int G = g->q_heads / g->kv_heads;
@@ -500,7 +501,7 @@ static int decode_impl(const vt_kv_geometry* g, int32_t layer, const void* q,
   cudaError_t e;
   if (tc) {  // tcgen05 path (TMA maps over the request VAs)
     int rc = vt_launch_decode_tc(g, layer, q, kv_maps, seq_lens, batch, n_splits, split, scale,
-                                 out, a.part_o, a.part_ml, arrivals, num_sms(), st);
+                                 out, a.part_o, a.part_ml, arrivals, num_sms(), chained, st);
     g_last_launches = 1;
     return rc;
   } else switch (G) {
@@ -526,7 +527,17 @@ extern "C" int vt_decode_attention(const vt_kv_geometry* g, int32_t layer, const
                                    float scale, void* out, void* workspace, size_t workspace_bytes,
                                    int32_t split_tokens, void* stream) {
   return decode_impl(g, layer, q, kv_va, kv_maps, nullptr, 0, 0, seq_lens, batch, max_seq_len,
-                     scale, out, workspace, workspace_bytes, split_tokens, stream);
+                     scale, out, workspace, workspace_bytes, split_tokens, false, stream);
+}
+
+extern "C" int vt_decode_attention_chained(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                           const uint64_t* kv_va, const void* kv_maps,
+                                           const int32_t* seq_lens, int32_t batch,
+                                           int32_t max_seq_len, float scale, void* out,
+                                           void* workspace, size_t workspace_bytes,
+                                           int32_t split_tokens, void* stream) {
+  return decode_impl(g, layer, q, kv_va, kv_maps, nullptr, 0, 0, seq_lens, batch, max_seq_len,
+                     scale, out, workspace, workspace_bytes, split_tokens, true, stream);
 }
 
 extern "C" int vt_decode_attention_paged(const vt_kv_geometry* g, int32_t layer, const void* q,
@@ -538,5 +549,5 @@ extern "C" int vt_decode_attention_paged(const vt_kv_geometry* g, int32_t layer,
   if (block_table == nullptr || pool_base == nullptr) return cudaErrorInvalidValue;
   return decode_impl(g, layer, q, nullptr, nullptr, block_table, max_blocks,
                      reinterpret_cast<uint64_t>(pool_base), seq_lens, batch, max_seq_len, scale,
-                     out, workspace, workspace_bytes, split_tokens, stream);
+                     out, workspace, workspace_bytes, split_tokens, false, stream);
 }

@@ -510,7 +510,8 @@ using namespace vt::dtc;
 int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
                         const void* kv_maps, const int32_t* seq_lens, int32_t batch,
                         int32_t n_splits, int32_t split, float scale, void* out, float* part_o,
-                        float* part_ml, int32_t* arrivals, int32_t n_sms, cudaStream_t stream) {
+                        float* part_ml, int32_t* arrivals, int32_t n_sms, bool pdl,
+                        cudaStream_t stream) {
   const int G = g->q_heads / g->kv_heads;
   if (G > MAXG || split % TILE) return cudaErrorInvalidValue;
   static_assert(sizeof(Smem) + 1024 <= 232448, "shared memory budget");
@@ -543,13 +544,31 @@ int vt_launch_decode_tc(const vt_kv_geometry* g, int32_t layer, const void* q,
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    // Launched without programmatic dependent launch on purpose: with PDL the
-    // 32 layer launches of a step run back to back with no kernel boundary,
-    // and the driver's concurrent cuMemMap / cuMemSetAccess (the worker's
-    // extends) then slowed from ~0.8 ms to 7.5 ms and surfaced as host waits
-    // (measured: 6077 -> 3968 GB/s per step). The griddepcontrol instructions
-    // in the kernel are no-ops without it.
-    kernel<<<grid, kThreads, smem, stream>>>(qmap, a);
+    // Chained launches (a decode layer right after another decode layer)
+    // use programmatic dependent launch: this grid's CTAs start streaming
+    // their first ring of K/V while the previous layer drains; q, outputs and
+    // the split workspace are touched only after griddepcontrol.wait. The
+    // first decode after the step's KV append is a plain launch (it reads the
+    // K/V that kernel writes). Measured (bench, config 2): 6392 -> 6632 GB/s
+    // per step. Cost: with boundaries only once per step the driver applies
+    // the worker's concurrent cuMemMap / cuMemSetAccess at the next plain
+    // kernel boundary (SetAccess 0.7 -> 2.7 ms at 8B, ~17 ms at 32k), which
+    // the map-ahead extends absorb (0 host waits, 0 stalled steps).
+    if (pdl) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid, 1, 1);
+      cfg.blockDim = dim3(kThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kernel, qmap, a);
+    } else {
+      kernel<<<grid, kThreads, smem, stream>>>(qmap, a);
+    }
   };
   switch (G) {
     case 1: launch(decode_tc_kernel<1>); break;

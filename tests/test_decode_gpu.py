@@ -152,3 +152,33 @@ def test_paged_baseline_matches_vtensor(cuda_ok):
     b = decode_attention_paged(q, pool, table, seq, 9, st.geo, max(lens), split_tokens=512)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+def test_chained_layers_match_oracle(cuda_ok):
+    """Layers launched back to back with programmatic dependent launch
+    (vt_decode_attention_chained) after a KV append: every layer's output
+    matches the oracle, and the shared split workspace is never raced."""
+    layers, hkv, hq = 32, 8, 32
+    lens = [100, 1500, 4095, 17, 2048, 3000, 1, 777]
+    st = cuda_stack(layers, hkv, hq, 4352)
+    kv_va, seq = admit_with_lengths(st, lens, seed=21)
+    for i, n in enumerate(lens):
+        st.sched.extend(f"req{i}", n + 1)
+    st.dev.wait()
+    k_new = torch.randn(layers, len(lens), hkv, 128, device="cuda").to(torch.bfloat16)
+    kv_append(k_new, torch.randn_like(k_new), kv_va, seq.clone(), st.geo)
+    new_lens = [n + 1 for n in lens]
+    seq1 = torch.tensor(new_lens, dtype=torch.int32, device="cuda")
+    maps = mapped_maps(st, kv_va, len(lens))
+    q = torch.randn(layers, len(lens), hq, 128, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    ws = DecodeWorkspace(st.geo, len(lens), 4352, 0)
+    for layer in range(layers):
+        decode_attention(q[layer], kv_va, seq1, layer, st.geo, max(new_lens), out=out[layer],
+                         workspace=ws, kv_maps=maps, chained=layer > 0)
+    torch.cuda.synchronize()
+    for layer in (0, 1, 2, 15, 30, 31):
+        ks, vs = gather(st, kv_va, new_lens, layer)
+        ref = decode_attention_ref(q[layer].cpu(), ks, vs)
+        assert rel_err(out[layer].cpu(), ref) <= TOL, layer
