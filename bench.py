@@ -4,23 +4,25 @@
 One *step* = one decode step of a Llama-3-8B-shaped batch (32 q / 8 kv heads,
 d 128, bf16, 32 layers, batch 64 per GPU, ~4k context) through the product path:
 
-  host : vTensor extend for the NEXT token of every request (VTS.extend ->
+  host : vTensor extend ahead of every request's next tokens (VTS.extend ->
          VTO.p_alloc/map_chunks -> libvtensor; cuMemCreate/cuMemMap/
          cuMemSetAccess run on the shim's worker thread, overlapping the GPU
          work already queued), wait(ticket) before the launch that writes the
          new pages, append_token bookkeeping;
   GPU  : vt_kv_append (new K/V of all 32 layers) + 32 x vt_decode_attention
-         (split-KV kernel + LSE combine).
+         (tcgen05 split-KV kernel with the split merge fused in its epilogue;
+         layers 2..32 chained with programmatic dependent launch).
 
-Context lengths are staggered (4081..4096 at start) so that every step some
-requests cross a 16-token chunk boundary and need a real 2 MiB chunk mapped.
+Context lengths are staggered over one map-ahead window so that every step
+some requests run low on headroom and extend by a run of real 2 MiB chunks.
 
 Metric (BASELINE.json): decode-attn KV GB/s = algorithmic bytes
 (KV read + q read + out write + appended K/V) / time; tokens/s and the extend
 latency are reported beside it. ``value`` is device-timed with inputs resident
 in HBM (KV working set 32 GiB >> 126 MB L2, so no flush is needed); ``e2e``
 repeats the run through the public API with q / new-K/V copied from pinned host
-memory and the outputs copied back inside the timed region.
+memory and the outputs copied back inside the timed region (copies pipelined
+on a side stream across steps, as a serving loop would).
 
 Multi-GPU (torchrun, one process per GPU): requests are partitioned — each GPU
 owns its own VMM chunk pool and its own 64 requests (weak scaling); there is no
