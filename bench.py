@@ -888,9 +888,29 @@ def manager_cpu_baseline(reference_only: bool = False) -> dict:
                     app.append(time.perf_counter_ns() - t0)
         ext.sort()
         app.sort()
+        # config 3's manager ops: record a 2048-token conversation prefix, then
+        # admit turns that rTree-match it (2048 shared + 512 new tokens)
+        rec, match = [], []
+        for c in range(4):
+            conv = [(c * 7919 + i) % 32000 for i in range(2048)]
+            sched.create(f"c{c}", conv)
+            sched.mark_prefilled(f"c{c}")
+            t0 = time.perf_counter_ns()
+            sched.prefix_record(f"c{c}")
+            rec.append(time.perf_counter_ns() - t0)
+            for t in range(4):
+                rid = f"c{c}t{t}"
+                t0 = time.perf_counter_ns()
+                sched.prefix_match(rid, conv + [(t * 31 + i) % 32000 for i in range(512)])
+                match.append(time.perf_counter_ns() - t0)
+                sched.release(rid)
+        rec.sort()
+        match.sort()
         out[name] = {"extend_1chunk_us_p50": round(ext[len(ext) // 2] / 1e3, 2),
                      "extend_1chunk_us_p99": round(ext[int(len(ext) * 0.99)] / 1e3, 2),
-                     "append_token_us_p50": round(app[len(app) // 2] / 1e3, 2)}
+                     "append_token_us_p50": round(app[len(app) // 2] / 1e3, 2),
+                     "prefix_record_2048_us_p50": round(rec[len(rec) // 2] / 1e3, 1),
+                     "prefix_match_2048_512_us_p50": round(match[len(match) // 2] / 1e3, 1)}
     out["cores"] = 1
     out["kind"] = "port"
     return out
