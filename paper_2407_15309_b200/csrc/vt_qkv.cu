@@ -21,16 +21,19 @@
 //   share of the weight is ONE contiguous byte range pulled with 16 KiB bulk
 //   copies (no tensor map, sequential DRAM pages).
 // * K split over a CTA pair (thread-block cluster of 2). Each feature tile is
-//   computed by two CTAs, one per half of `hidden`; the upper CTA stages its
-//   fp32 partial in its own (by then idle) ring and ONE bulk copy moves it
-//   into the lower CTA's ring over distributed shared memory, completing on
-//   the lower CTA's mbarrier; the lower CTA adds it and stores. The reduction
-//   never touches global memory. Measured alternatives (tools/trace_qkv.py
+//   computed by two CTAs, one per half of `hidden`; once the lower CTA's MMAs
+//   are done (its ring is idle) the upper CTA writes its fp32 partial straight
+//   from TMEM into that ring with asynchronous remote stores (st.async over
+//   distributed shared memory, each completing its bytes on the lower CTA's
+//   mbarrier); the lower CTA adds it and stores. The reduction never touches
+//   global memory. Measured alternatives (tools/trace_qkv.py
 //   timelines): a global split-K reduction (fp32 partials in L2 + arrival
 //   counter) with a stream-K split over every SM streamed the weight at
 //   6.9 TB/s but its chain of L2 round trips (~1 us each under load) added a
-//   5-6 us tail; per-thread DSMEM stores of the partial took 1.4 us (scalar,
-//   coalesced) / 2.3 us (16-byte, strided) against 0.8 us for the bulk copy.
+//   5-6 us tail; synchronous per-thread DSMEM stores of the partial took
+//   1.4 us (scalar, coalesced) / 2.3 us (16-byte, strided); staging it in the
+//   upper CTA's own ring for one bulk copy took 1.5 us and ran the same as
+//   st.async end to end (12.7 us/layer).
 //   Clusters of 2 all co-schedule (74 at one CTA per SM; clusters of 3 do
 //   not: 45 < 48 tiles).
 //
@@ -93,19 +96,6 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
-}
-// Bulk copy of `bytes` from this CTA's shared memory into a peer CTA's,
-// completing on the peer's mbarrier (SASS UBLKCP over DSMEM).
-__device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, const void* src, uint32_t bytes,
-                                            uint32_t bar_cluster) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst_cluster), "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
-      : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void arrive_peer(uint32_t bar_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_addr)
@@ -241,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // this thread's output feature within the tile
     const int ep = threadIdx.x - 64;      // 0..127
-    float* peer_part = reinterpret_cast<float*>(ring);  // [NT][BM] fp32 partial (both CTAs)
+    float* peer_part = reinterpret_cast<float*>(ring);  // [NT][BM] fp32 partial (lower CTA)
     if (half == 0) {
       const int kind = m < a.hq ? 0 : (m < a.hq + a.hkv ? 1 : 2);  // q | K | V
       const int head = kind == 0 ? m : (kind == 1 ? m - a.hq : m - a.hq - a.hkv);
@@ -270,9 +260,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ep == 0) QKV_TRACE(6);
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     if (KS == 2 && half == 1) {
-      // upper half: stage the fp32 partial [NT][BM] in our own ring (free:
-      // our MMAs are done), then one bulk copy into the lower CTA's ring once
-      // its MMAs are done too, completing on its barrier
+      // upper half: once the lower CTA's MMAs are done (its ring is free),
+      // asynchronous remote stores of the fp32 partial straight from the
+      // accumulator, each completing its bytes on the lower CTA's barrier
+      mbar_wait(&peer_ready, 0);
+      if (ep == 0) QKV_TRACE(7);
+      const uint32_t dst = peer_addr(peer_part, 0);
+      const uint32_t bar = peer_addr(&partial_full, 0);
 #pragma unroll 1
       for (int c = 0; c < NT; c += 32) {
         uint32_t r0[16], r1[16];
@@ -281,19 +275,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::wait_ld();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          peer_part[(c + i) * BM + row] = __uint_as_float(r0[i]);
-          peer_part[(c + 16 + i) * BM + row] = __uint_as_float(r1[i]);
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                           dst + ((c + i) * BM + row) * 4),
+                       "r"(r0[i]), "r"(bar)
+                       : "memory");
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                           dst + ((c + 16 + i) * BM + row) * 4),
+                       "r"(r1[i]), "r"(bar)
+                       : "memory");
         }
       }
-      fence_proxy_async_smem();  // generic-proxy writes -> the bulk copy's reads
-      named_bar_sync(1, 128);
-      if (ep == 0) {
-        mbar_wait(&peer_ready, 0);
-        QKV_TRACE(7);
-        bulk_s2peer(peer_addr(peer_part, 0), peer_part, NT * BM * 4, peer_addr(&partial_full, 0));
-        bulk_wait_read();  // our shared memory must outlive the copy's reads
-        QKV_TRACE(8);
-      }
+      if (ep == 0) QKV_TRACE(8);
     } else {
       if (KS == 2) {
         if (ep == 0) {
