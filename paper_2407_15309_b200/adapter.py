@@ -142,39 +142,107 @@ class GpuCompute:
     def _va(self, rid: str) -> int:
         return self.dev.va(self.adapter.scheduler.mem[rid].vt.space.rng)
 
-    def step(self, rids: list[str], q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
-             out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None):
-        from .attention import decode_attention, kv_append, last_launches
-
+    def _batch(self, rids: list[str], device, stream):
+        """Device-side tables of a decode batch: VAs, positions of the new
+        token (= token_count), lengths including it, TMA descriptors."""
         sched = self.adapter.scheduler
         tpc = self.adapter.config.tokens_per_chunk
         B = len(rids)
+        if B > self.max_batch:
+            raise ValueError("batch exceeds max_batch")
         lens = [sched.mem[r].vt.token_count for r in rids]
         for r, n in zip(rids, lens):
             if sched.mem[r].vt.space.mapped_pages * tpc < n + 1:
                 raise RuntimeError(f"{r}: no capacity for token {n}; call ensure_capacity first")
         self.dev.wait()  # every page this step touches has been mapped by the worker
         vas = [self._va(r) for r in rids]
-        stream = stream or torch.cuda.current_stream()
-        dev_idx = q.device
-        kv_va = torch.tensor(vas, dtype=torch.int64).to(dev_idx, non_blocking=True)
-        pos = torch.tensor(lens, dtype=torch.int32).to(dev_idx, non_blocking=True)
-        seq = pos + 1
-        if B > self.max_batch:
-            raise ValueError("batch exceeds max_batch")
+        kv_va = torch.tensor(vas, dtype=torch.int64).to(device, non_blocking=True)
+        pos = torch.tensor(lens, dtype=torch.int32).to(device, non_blocking=True)
         pad = self.max_batch - B
         maps = self.maps.update(vas + [vas[0]] * pad,
                                 [-(-(n + 1) // tpc) * tpc for n in lens] + [lens[0] + 1] * pad,
                                 stream)[: B * 128]
+        return kv_va, pos, pos + 1, maps, max(lens) + 1
+
+    def step(self, rids: list[str], q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+             out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None):
+        from .attention import decode_attention, kv_append, last_launches
+
+        stream = stream or torch.cuda.current_stream()
+        kv_va, pos, seq, maps, mx = self._batch(rids, q.device, stream)
         kv_append(k_new, v_new, kv_va, pos, self.geo, stream=stream)
         self.launches += 1
         if out is None:
             out = torch.empty_like(q)
-        mx = max(lens) + 1
         for layer in range(q.shape[0]):
             decode_attention(q[layer], kv_va, seq, layer, self.geo, mx, out=out[layer],
                              workspace=self.ws, split_tokens=self.split, kv_maps=maps,
                              stream=stream, chained=layer > 0)
             self.launches += last_launches()
+        self.dev.fence(stream.cuda_stream)
+        return out
+
+    def step_from_hidden(self, rids: list[str], x: torch.Tensor, w_qkv: list,
+                         out: torch.Tensor | None = None,
+                         stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """A decode step whose new token's q / K / V come from the fused QKV
+        projection: per layer, ``x[l]`` ``[B, hidden]`` through
+        ``w_qkv[l]`` (:class:`PackedQKVWeight`) writes K/V at ``token_count``
+        straight into the cache (vt_qkv_append), then attention reads
+        ``token_count + 1`` tokens. Returns ``[L, B, Hq, d]``."""
+        from .attention import decode_attention, last_launches, qkv_append
+
+        stream = stream or torch.cuda.current_stream()
+        L, B, _ = x.shape
+        kv_va, pos, seq, maps, mx = self._batch(rids, x.device, stream)
+        tok_req = torch.arange(B, dtype=torch.int32, device=x.device)
+        if out is None:
+            out = torch.empty(L, B, self.geo.q_heads, self.geo.head_dim, dtype=torch.bfloat16,
+                              device=x.device)
+        for layer in range(L):
+            q = qkv_append(x[layer], w_qkv[layer], tok_req, pos, kv_va, self.geo, layer,
+                           stream=stream)
+            # plain launch: it reads the K/V the projection just wrote
+            decode_attention(q, kv_va, seq, layer, self.geo, mx, out=out[layer],
+                             workspace=self.ws, split_tokens=self.split, kv_maps=maps,
+                             stream=stream)
+            self.launches += 1 + last_launches()
+        self.dev.fence(stream.cuda_stream)
+        return out
+
+    def prefill(self, rid: str, x: torch.Tensor, w_qkv: list, start: int,
+                stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Prefill / prefix-prefill of request ``rid``: its new tokens sit at
+        ``[start, start + n_new)`` (``start`` = tokens already in the cache,
+        e.g. an rTree-shared prefix mapped by identity). Per layer, ``x[l]``
+        ``[n_new, hidden]`` goes through the fused projection, which writes the
+        new tokens' K/V into the cache (vt_qkv_append), then the new tokens
+        attend causally to ``[0, start + i]`` (vt_prefill_attention). The pages
+        of ``[0, start + n_new)`` must be mapped (admission / prefill_reserve).
+        Returns ``[L, n_new, Hq, d]``; the caller then ``mark_prefilled``."""
+        from .attention import kv_tensor_maps, last_launches, prefill_attention, qkv_append
+
+        stream = stream or torch.cuda.current_stream()
+        L, n_new, _ = x.shape
+        rm = self.adapter.scheduler.mem[rid]
+        tpc = self.adapter.config.tokens_per_chunk
+        if rm.vt.space.mapped_pages * tpc < start + n_new:
+            raise RuntimeError(f"{rid}: tokens [0, {start + n_new}) are not all mapped")
+        self.dev.wait()
+        va = self._va(rid)
+        dev = x.device
+        kv_va = torch.tensor([va], dtype=torch.int64, device=dev)
+        tok_req = torch.zeros(n_new, dtype=torch.int32, device=dev)
+        tok_pos = torch.arange(start, start + n_new, dtype=torch.int32, device=dev)
+        maps = kv_tensor_maps([va], [start + n_new], self.geo)
+        st = torch.tensor([start], dtype=torch.int32, device=dev)
+        out = torch.empty(L, n_new, self.geo.q_heads, self.geo.head_dim, dtype=torch.bfloat16,
+                          device=dev)
+        for layer in range(L):
+            q = qkv_append(x[layer], w_qkv[layer], tok_req, tok_pos, kv_va, self.geo, layer,
+                           stream=stream)
+            prefill_attention(q.unsqueeze(0), maps, st, layer, self.geo, out=out[layer].unsqueeze(0),
+                              stream=stream)
+            self.launches += 1 + last_launches()
         self.dev.fence(stream.cuda_stream)
         return out
