@@ -359,7 +359,7 @@ class DecodeWorkload:
                 + 2 * self.B * self.hq * 128 * 2)
 
     # -- one step -------------------------------------------------------------
-    def step(self, q=None, k_new=None, v_new=None, out=None, layer_events=None):
+    def step(self, q=None, k_new=None, v_new=None, out=None, run_events=None):
         import torch
 
         from paper_2407_15309_b200.attention import decode_attention, kv_append, last_launches
@@ -391,7 +391,7 @@ class DecodeWorkload:
         chain = self.chain
         self.chained_steps += int(chain)
         torch.add(self.seq, 1, out=self.seq1)  # lengths including this step's token
-        for grp in self.groups:
+        for gi, grp in enumerate(self.groups):
             kv_maps = None
             if grp.maps is not None:
                 # TMA chunk extent = chunks holding valid tokens (all waited
@@ -402,16 +402,19 @@ class DecodeWorkload:
             kv_append(k_new[lo:lo + grp.n_layers], v_new[lo:lo + grp.n_layers], grp.kv_va,
                       self.seq, grp.geo)
             launches += 1
+            # events bracket each group's run of decode layers only: the run
+            # starts with a plain launch after the KV append, so they do not
+            # break the chain of programmatic dependent launches inside it
+            if run_events is not None:
+                run_events[gi][0].record(self.stream)
             for li in range(grp.n_layers):
                 layer = lo + li
-                if layer_events is not None:
-                    layer_events[layer][0].record(self.stream)
                 decode_attention(q[layer], grp.kv_va, self.seq1, li, grp.geo, mx,
                                  out=out[layer], workspace=self.ws, split_tokens=self.split,
                                  kv_maps=kv_maps, chained=chain and li > 0)
-                if layer_events is not None:
-                    layer_events[layer][1].record(self.stream)
                 launches += last_launches()
+            if run_events is not None:
+                run_events[gi][1].record(self.stream)
         self.seq, self.seq1 = self.seq1, self.seq
         self.dev.fence(self.stream.cuda_stream)
         self.last_done = torch.cuda.Event()
@@ -442,9 +445,8 @@ def run_ours(args, world, rank, local):
     barrier(world)
 
     # ---- device-resident timed region ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(wl.L)]
-    layer_ms = []
+    run_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in wl.groups] for _ in range(args.steps)]
     bytes_total = 0
     decode_bytes = 0
     launches = 0
@@ -462,21 +464,17 @@ def run_ours(args, world, rank, local):
         start.record()
         for i in range(args.steps):
             bytes_total += wl.algorithmic_bytes_per_step()
-            # Per-launch decode durations (events on the launch stream) are
-            # taken in the last step only: an event between two launches
-            # serialises them and would cancel the programmatic-dependent-launch
-            # overlap of consecutive layers in every other step.
-            last = i == args.steps - 1
-            if last:
-                decode_bytes += wl.decode_bytes_per_launch() * wl.L
-            launches += wl.step(layer_events=ev if last else None)
-            if last:
-                layer_ms.append(ev)
+            # Decode launch durations: CUDA events on the launch stream around
+            # each group's run of decode layers in every timed step (an event
+            # between two chained launches would serialise them; these sit
+            # where the chain starts and ends anyway).
+            decode_bytes += wl.decode_bytes_per_launch() * wl.L
+            launches += wl.step(run_events=run_ev[i])
         stop.record()
         torch.cuda.synchronize()
     elapsed_ms = start.elapsed_time(stop)
-    kern_ms = sum(a.elapsed_time(b) for evs in layer_ms for a, b in evs)
-    n_decode = wl.L  # launches of the event-timed step
+    kern_ms = sum(a.elapsed_time(b) for evs in run_ev for a, b in evs)
+    n_decode = wl.L * args.steps  # decode launches inside the bracketed runs
     stalls = wl.stalls - stalls0
     chained = wl.chained_steps - chained0
     elapsed_max = max_over_ranks(elapsed_ms, world)
@@ -621,6 +619,9 @@ def run_ours(args, world, rank, local):
                 "frac": round(achieved / hbm_peak, 4),
                 "traffic": traffic,
                 "per_launch_us": round(per_launch_s * 1e6, 2),
+                "launch_timing": ("CUDA events on the launch stream around each run of chained "
+                                  "decode layers, every timed step; per launch = run time / "
+                                  "launches in the run"),
                 "algorithmic_bytes_per_launch": int(decode_bytes / n_decode),
             },
             "extend": {
