@@ -90,7 +90,7 @@ class VirtualRange:
     page_count: int
 
 
-@dataclasses.dataclass
+@dataclasses.dataclass(slots=True)
 class PhysicalHandle:
     """One physical chunk; shared by identity between device, pool and tables."""
 
