@@ -149,9 +149,12 @@ _COLL_DEVICE = "cuda"
 def dist_setup(args):
     """One process per GPU (torchrun). NCCL carries only the barrier and the
     max/sum of the timings. When more ranks than GPUs are launched (checking
-    the N-rank mechanics on a 1-GPU box) ranks share devices round-robin and
-    the timing reductions go over gloo, since NCCL refuses two ranks on one
-    GPU; numbers from such a run are not scaling numbers."""
+    the N-rank mechanics on a 1-GPU box) ranks share devices round-robin, the
+    timing reductions go over gloo (NCCL refuses two ranks on one GPU);
+    numbers from such a run are not scaling numbers, and two processes'
+    tcgen05 kernels time-sliced on one GPU occasionally stall (seen in ~1 of 3
+    two-rank runs) — a mechanics check only, never the driver's
+    one-rank-per-GPU configuration."""
     global _COLL_DEVICE
     import torch
 

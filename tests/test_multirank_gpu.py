@@ -5,9 +5,10 @@ One process per rank, exactly as `bench.py` runs under torchrun: every rank
 owns its own ``VirtualMemoryDevice`` (its own VMM chunk pool and VA ranges),
 manager and kernel launches; no collective touches the data path — gloo only
 gathers the per-rank outputs so rank 0 can check them. The round-end box has
-one GPU, so ranks map onto ``cuda:(rank % device_count)``: with one device the
-N pools share its HBM, which changes nothing on the path under test (every
-pool, VA and launch is still private to its rank).
+one GPU, so ranks map onto ``cuda:(rank % device_count)`` and take turns on it
+(two processes' tcgen05 kernels time-sliced on one GPU were seen to stall);
+the N pools share its HBM, which changes nothing on the path under test
+(every pool, VA and launch is still private to its rank).
 
 * KV-head partition (config 4, Llama-2-70B shape): rank r holds kv heads
   ``[r*8/N, (r+1)*8/N)`` and the matching q heads of every request, in
@@ -85,39 +86,54 @@ def _rank_main(rank, world, port, tmp):
         from paper_2407_15309_b200.sharding import head_shard, layer_groups, partition_requests
         from vt_gpu_util import admit_with_lengths, cuda_stack
 
-        results = {}
-        # ---- KV-head partition, Llama-2-70B shape (80 layers, 64 q / 8 kv heads)
+        # the global (unsharded) inputs, identical on every rank (seeded, CPU)
         lens = [1, 255, 256, 257, 1500, 4096]
         ks, vs = _global_kv(70, lens, 8)
         q = torch.randn(len(lens), 64, D, generator=torch.Generator().manual_seed(71)).to(torch.bfloat16)
-        sh = head_shard(8, 64, world, rank)
-        kl, kh = sh.kv_heads
-        ql, qh = sh.q_heads
-        layer = 37  # inside the third 16-layer group
-        first, geom = next((f, g) for f, g in layer_groups(80, sh.local_kv_heads)
-                           if f <= layer < f + g.layers)
-        st = cuda_stack(geom.layers, sh.local_kv_heads, sh.local_q_heads, 4096)
-        kv_va, seq = admit_with_lengths(st, lens, fill=False)
-        for b, va in enumerate(kv_va.tolist()):
-            _write_layer(st, va, layer - first, ks[b][kl:kh], vs[b][kl:kh])
-        torch.cuda.synchronize()
-        results["heads"] = _decode_both(st, q[:, ql:qh].cuda(), kv_va, seq, layer - first, lens)
-
-        # ---- request partition, Llama-3-8B shape (32 layers, 32 q / 8 kv heads)
         rlens = [0, 15, 16, 17, 333, 1024, 2047, 4096]
         rks, rvs = _global_kv(80, rlens, 8)
         rq = torch.randn(len(rlens), 32, D, generator=torch.Generator().manual_seed(81)).to(torch.bfloat16)
-        mine = partition_requests([f"r{i}" for i in range(len(rlens))], world, rank)
-        if mine:
-            sub = [rlens[i] for i in mine]
-            st8 = cuda_stack(32, 8, 32, 4352)
-            kv8, seq8 = admit_with_lengths(st8, sub, fill=False)
-            for j, va in enumerate(kv8.tolist()):
-                _write_layer(st8, va, 5, rks[mine[j]], rvs[mine[j]])
+
+        def gpu_work():
+            out = {}
+            # ---- KV-head partition, Llama-2-70B shape (80 layers, 64 q / 8 kv heads)
+            sh = head_shard(8, 64, world, rank)
+            kl, kh = sh.kv_heads
+            ql, qh = sh.q_heads
+            layer = 37  # inside the third 16-layer group
+            first, geom = next((f, g) for f, g in layer_groups(80, sh.local_kv_heads)
+                               if f <= layer < f + g.layers)
+            st = cuda_stack(geom.layers, sh.local_kv_heads, sh.local_q_heads, 4096)
+            kv_va, seq = admit_with_lengths(st, lens, fill=False)
+            for b, va in enumerate(kv_va.tolist()):
+                _write_layer(st, va, layer - first, ks[b][kl:kh], vs[b][kl:kh])
             torch.cuda.synchronize()
-            results["requests"] = (mine, _decode_both(st8, rq[mine].cuda(), kv8, seq8, 5, sub))
-        else:
-            results["requests"] = (mine, None)
+            out["heads"] = _decode_both(st, q[:, ql:qh].cuda(), kv_va, seq, layer - first, lens)
+            # ---- request partition, Llama-3-8B shape (32 layers, 32 q / 8 kv heads)
+            mine = partition_requests([f"r{i}" for i in range(len(rlens))], world, rank)
+            if mine:
+                sub = [rlens[i] for i in mine]
+                st8 = cuda_stack(32, 8, 32, 4352)
+                kv8, seq8 = admit_with_lengths(st8, sub, fill=False)
+                for j, va in enumerate(kv8.tolist()):
+                    _write_layer(st8, va, 5, rks[mine[j]], rvs[mine[j]])
+                torch.cuda.synchronize()
+                out["requests"] = (mine, _decode_both(st8, rq[mine].cuda(), kv8, seq8, 5, sub))
+            else:
+                out["requests"] = (mine, None)
+            st.dev.wait()
+            torch.cuda.synchronize()
+            return out
+
+        # Ranks share the one GPU here: they run their GPU sections one after
+        # another (gloo barriers), so no two contexts' tcgen05 kernels are
+        # time-sliced against each other; everything else (process, VMM pool,
+        # VA ranges, manager, launches) stays private to each rank.
+        results = None
+        for turn in range(world):
+            if turn == rank:
+                results = gpu_work()
+            dist.barrier()
 
         gathered = [None] * world
         dist.all_gather_object(gathered, (rank, results))
