@@ -251,7 +251,8 @@ class DecodeWorkload:
     """
 
     def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05",
-                 world: int = 1, rank: int = 0, premap_steps: int = 0, chain: bool = True):
+                 world: int = 1, rank: int = 0, premap_steps: int = 0, chain: bool = True,
+                 total_steps: int = 64):
         import torch
 
         import paper_2407_15309_b200 as vt
@@ -265,13 +266,14 @@ class DecodeWorkload:
             hkv, hq = sh.local_kv_heads, sh.local_q_heads
         self.L, self.hkv, self.hq, self.B, self.ctx = L, hkv, hq, B, ctx
         self.path = path
-        self.max_seq = ctx + 1024
+        # every request grows by one token per step: reserve for the whole run
+        self.max_seq = ctx + 1024 + total_steps
         self.dev = vt.VirtualMemoryDevice(
             vt.DeviceConfig(capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB),
             cuda_ordinal=torch.cuda.current_device())
         groups = layer_groups(L, hkv)
         tpc = 2 * MIB // groups[0][1].bytes_per_token
-        self.map_ahead = 4         # chunks mapped per extend: one cuMemSetAccess per run
+        self.map_ahead = int(os.environ.get("VT_MAP_AHEAD", "4"))  # chunks per extend: one cuMemSetAccess per run
         # extend once headroom drops below this many chunks: with chained
         # layers the driver may take several steps to complete a mapping
         self.chain = chain
@@ -436,7 +438,7 @@ def run_ours(args, world, rank, local):
     total_steps = args.warmup + 2 * args.steps + 2
     wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
                         world=world, rank=rank, premap_steps=total_steps if args.premap else 0,
-                        chain=not args.no_chain)
+                        chain=not args.no_chain, total_steps=total_steps)
     if args.profile_steps:
         for _ in range(args.profile_steps):
             wl.step()
