@@ -318,8 +318,13 @@ class DecodeWorkload:
     # -- manager half ---------------------------------------------------------
     def _prewarm(self, chunks: int):
         """Warm each group's pSet free list (lazy deallocation, ops.py:150-178):
-        admit and release placeholder requests so steady-state extends reuse
-        parked chunks instead of paying cuMemCreate under load."""
+        admit and release placeholder requests one after another so steady
+        state extends reuse parked chunks instead of paying cuMemCreate under
+        load. Each placeholder reuses its predecessor's chunks, so the list
+        ends at one space's worth (e.g. 320 chunks at 8B) while `chunks` are
+        cycled through the driver. (Holding all placeholders before releasing
+        them — 1024 parked chunks — was measured to make the worker's
+        cuMemSetAccess 5-10x slower in the timed region, so it stays this way.)"""
         for grp in self.groups:
             per = self.max_seq // grp.tpc
             left, i = chunks // len(self.groups), 0
