@@ -82,6 +82,20 @@ def parse():
                     help="skip the fused QKV-projection + KV-append probe")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="run N untimed steps only (for ncu), print nothing")
+    ap.add_argument("--growth", action="store_true",
+                    help="config 5 growth trace: 16 requests decode from 256 to 32,752 tokens "
+                         "(32,496 steps, every chunk mapped on demand); --steps is ignored "
+                         "unless --growth-steps caps it")
+    ap.add_argument("--growth-steps", type=int, default=0,
+                    help="cap the growth trace at this many timed steps (0 = the full trace)")
+    ap.add_argument("--phys-reserve", type=int, default=-1,
+                    help="pre-created physical handles kept by the shim (-1 = auto: the chunks "
+                         "the run will create, capped at 16 GiB; 0 = off)")
+    ap.add_argument("--driver-threads", type=int, default=0,
+                    help="shim threads executing driver VMM ops in parallel (0 = library default)")
+    ap.add_argument("--check", action="store_true",
+                    help="after the timed region, compare sampled (request, layer) outputs of the "
+                         "last step (and the config-3 prefill probe) with the CPU oracle")
     return ap.parse_args()
 
 
@@ -252,7 +266,8 @@ class DecodeWorkload:
 
     def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05",
                  world: int = 1, rank: int = 0, premap_steps: int = 0, chain: bool = True,
-                 total_steps: int = 64):
+                 total_steps: int = 64, start_len: int = 0, max_seq: int = 0,
+                 phys_reserve: int = -1, driver_threads: int = 0):
         import torch
 
         import paper_2407_15309_b200 as vt
@@ -267,22 +282,29 @@ class DecodeWorkload:
         self.L, self.hkv, self.hq, self.B, self.ctx = L, hkv, hq, B, ctx
         self.path = path
         # every request grows by one token per step: reserve for the whole run
-        self.max_seq = ctx + 1024 + total_steps
+        self.max_seq = max_seq or ctx + 1024 + total_steps
         self.dev = vt.VirtualMemoryDevice(
             vt.DeviceConfig(capacity_bytes=160 * GIB, chunk_size_bytes=2 * MIB),
             cuda_ordinal=torch.cuda.current_device())
+        if driver_threads:
+            self.dev.set_driver_threads(driver_threads)
         groups = layer_groups(L, hkv)
         tpc = 2 * MIB // groups[0][1].bytes_per_token
-        self.map_ahead = int(os.environ.get("VT_MAP_AHEAD", "4"))  # chunks per extend: one cuMemSetAccess per run
-        # extend once headroom drops below this many chunks: with chained
-        # layers the driver may take several steps to complete a mapping
+        self.map_ahead = int(os.environ.get("VT_MAP_AHEAD", "4"))  # chunks per extend call
+        # extend once headroom drops below this many chunks: a mapping takes
+        # 0.15-2 ms of driver time per chunk (tools/vmm_probe.cu), i.e. a few
+        # steps when several requests cross a chunk edge together
         self.chain = chain
-        self.lead_chunks = 3 if chain else 1
+        self.lead_chunks = int(os.environ.get("VT_LEAD_CHUNKS", "3" if chain else "1"))
         win = self.map_ahead * tpc
         self.rids = [f"r{b}" for b in range(B)]
-        # staggered lengths over one map-ahead window: every step some request
-        # runs out of headroom and extends by a `map_ahead`-chunk run
-        self.lens = [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx for b in range(B)]
+        if start_len:  # growth trace: every request starts at the same length
+            self.lens = [start_len] * B
+        else:
+            # staggered lengths over one map-ahead window: every step some
+            # request runs out of headroom and extends by a `map_ahead` run
+            self.lens = [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx
+                         for b in range(B)]
         self.groups = [_Group(self, first, geom, seed + 17 * i)
                        for i, (first, geom) in enumerate(groups)]
         gen = torch.Generator(device="cuda").manual_seed(seed)
@@ -298,11 +320,20 @@ class DecodeWorkload:
         self.host_lens = list(self.lens)
         self.stalls = 0
         self.host_waits = 0
+        self.host_wait_ns = 0
         self.chained_steps = 0
         self.last_done = None
+        self.gap_events: list | None = None  # (previous step's end, this step's start)
         self.extend_ns: list[int] = []
         self.chunks_mapped = 0
         self._prewarm(1024)
+        if phys_reserve < 0:  # auto: the chunks this run will still have to create
+            grow = sum(-(-(n + total_steps + (self.map_ahead + self.lead_chunks + 1) * tpc) // tpc)
+                       for n in self.lens) * len(groups)
+            phys_reserve = min(max(0, grow - 1024), 8192)
+        self.phys_reserve = phys_reserve
+        if phys_reserve:
+            self.dev.set_phys_reserve(phys_reserve)
         for grp in self.groups:  # staggered initial headroom (0..win-1 tokens)
             for b, rid in enumerate(self.rids):
                 extra = (premap_steps + win if premap_steps
@@ -386,10 +417,22 @@ class DecodeWorkload:
                     ticket = max(ticket, grp.chunk_ticket.pop((b, n // grp.tpc), 0))
         if ticket and not self.dev.ready(ticket):
             self.host_waits += 1
-            if self.last_done is not None and self.last_done.query():
-                self.stalls += 1  # GPU drained while this step's pages were still mapping
-        if ticket:
+            t0 = time.perf_counter_ns()
             self.dev.wait(ticket)
+            self.host_wait_ns += time.perf_counter_ns() - t0
+            # queried after the wait: the GPU ran dry while this step's pages
+            # were still mapping (the previous step's work had all finished)
+            if self.last_done is not None and self.last_done.query():
+                self.stalls += 1
+        elif ticket:
+            self.dev.wait(ticket)
+        if self.gap_events is not None and self.last_done is not None:
+            # device-side idle gap between the previous step's last kernel and
+            # this step's first one (events at the step boundary only, where
+            # the stream has a plain launch anyway)
+            st = torch.cuda.Event(enable_timing=True)
+            st.record(self.stream)
+            self.gap_events.append((self.last_done, st))
         mx = max(self.host_lens) + 1
         launches = 1
         # Decode layers after the first are chained (programmatic dependent
@@ -427,7 +470,7 @@ class DecodeWorkload:
                 run_events[gi][1].record(self.stream)
         self.seq, self.seq1 = self.seq1, self.seq
         self.dev.fence(self.stream.cuda_stream)
-        self.last_done = torch.cuda.Event()
+        self.last_done = torch.cuda.Event(enable_timing=self.gap_events is not None)
         self.last_done.record(self.stream)
         for grp in self.groups:
             for rid in self.rids:
@@ -437,22 +480,78 @@ class DecodeWorkload:
         return launches
 
 
+GROWTH_START, GROWTH_END = 256, 32752  # config 5: 32,496 decode steps
+
+
+def check_decode(wl, samples: int = 8, tol: float = 2e-2) -> dict:
+    """--check: the last timed step's outputs for `samples` (request, layer)
+    pairs — spread over the batch, the layers and the layer groups — against
+    the CPU oracle (oracle/attention_ref.py) over the same bf16 KV bytes read
+    back from the request VAs. Run after the timed region, outside it. The
+    tolerance is north_star's 2e-2 relative (bf16 in, fp32 accumulate)."""
+    import torch
+
+    from oracle.attention_ref import decode_attention_ref, rel_err
+    from paper_2407_15309_b200.kv_layout import read_kv
+
+    torch.cuda.synchronize()
+    picks = []
+    for i in range(samples):
+        b = (i * 37 + 5) % wl.B
+        layer = (i * (wl.L // samples) + i) % wl.L
+        picks.append((b, layer))
+    picks.append((wl.B - 1, wl.L - 1))
+    worst, rows = 0.0, []
+    for b, layer in picks:
+        gi = max(i for i, g in enumerate(wl.groups) if g.first <= layer)
+        grp = wl.groups[gi]
+        n = wl.host_lens[b]  # valid tokens the last step attended (incl. its own)
+        k, v = read_kv(grp.vas[b], n, layer - grp.first, grp.geo)
+        ref = decode_attention_ref(wl.q[layer, b:b + 1].cpu(), [k.cpu()], [v.cpu()])
+        err = rel_err(wl.out[layer, b:b + 1].cpu(), ref)
+        worst = max(worst, err)
+        rows.append({"request": b, "layer": layer, "len": n, "rel_err": round(err, 5)})
+    return {"oracle": "oracle/attention_ref.py decode_attention_ref (fp32/fp64 CPU)",
+            "samples": rows, "max_rel_err": round(worst, 5), "tol": tol, "ok": worst <= tol,
+            "split_tokens": wl.split or "auto"}
+
+
 def run_ours(args, world, rank, local):
     import torch
 
-    total_steps = args.warmup + 2 * args.steps + 2
-    wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
-                        world=world, rank=rank, premap_steps=total_steps if args.premap else 0,
-                        chain=not args.no_chain, total_steps=total_steps)
+    if args.growth:
+        args.config = "llama3-8b-32k"
+        trace = GROWTH_END - GROWTH_START
+        args.steps = min(trace - args.warmup, args.growth_steps or trace)
+        args.no_e2e = True  # the e2e pass would need a second growth trace
+        total_steps = args.warmup + args.steps
+        wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
+                            world=world, rank=rank,
+                            premap_steps=total_steps if args.premap else 0,
+                            chain=not args.no_chain, total_steps=total_steps,
+                            start_len=GROWTH_START, max_seq=32768,
+                            phys_reserve=0 if args.premap else args.phys_reserve,
+                            driver_threads=args.driver_threads)
+    else:
+        total_steps = args.warmup + 2 * args.steps + 2
+        wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
+                            world=world, rank=rank,
+                            premap_steps=total_steps if args.premap else 0,
+                            chain=not args.no_chain, total_steps=total_steps,
+                            phys_reserve=0 if args.premap else args.phys_reserve,
+                            driver_threads=args.driver_threads)
+    wl.dev.wait()  # the physical reserve (if any) is filled before any timing
     if args.profile_steps:
         for _ in range(args.profile_steps):
             wl.step()
         torch.cuda.synchronize()
         return
+    wl.gap_events = []
     for _ in range(args.warmup):
         wl.step()
     torch.cuda.synchronize()
     barrier(world)
+    wl.gap_events = []
 
     # ---- device-resident timed region ----
     run_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -462,6 +561,7 @@ def run_ours(args, world, rank, local):
     launches = 0
     stalls0 = wl.stalls
     waits0 = wl.host_waits
+    wait_ns0 = wl.host_wait_ns
     chained0 = wl.chained_steps
     drv0 = wl.dev.driver_stats()
     wl.dev.driver_latencies("map_page", reset=True)
@@ -484,6 +584,11 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
     elapsed_ms = start.elapsed_time(stop)
     kern_ms = sum(a.elapsed_time(b) for evs in run_ev for a, b in evs)
+    gaps = [a.elapsed_time(b) for a, b in wl.gap_events]
+    wl.gap_events = None
+    check = None
+    if args.check:
+        check = check_decode(wl)
     n_decode = wl.L * args.steps  # decode launches inside the bracketed runs
     stalls = wl.stalls - stalls0
     chained = wl.chained_steps - chained0
@@ -570,9 +675,10 @@ def run_ours(args, world, rank, local):
     per_launch_s = kern_ms * 1e-3 / n_decode
     achieved = (decode_bytes / n_decode) / per_launch_s / 1e9
     traffic = None
-    try:  # from the committed ncu --set full capture of this kernel (per launch)
+    traffic_key = f"{'growth' if args.growth else args.config}/{args.path}"
+    try:  # the committed ncu --set full capture of THIS config's kernel (per launch), if any
         prof = json.load(open(os.path.join(REPO, "profiles", "decode_traffic.json")))
-        traffic = prof[args.path]["dram_bytes_per_launch"]
+        traffic = prof[traffic_key]["dram_bytes_per_launch"]
     except Exception:
         pass
 
@@ -581,7 +687,7 @@ def run_ours(args, world, rank, local):
         cpu = cpu_baseline(args.config, budget_s=8.0)
     prefill = None
     if rank == 0 and not args.no_prefill and args.config == "llama3-8b-decode":
-        prefill = prefill_probe()
+        prefill = prefill_probe(check=args.check, cpu=not args.no_cpu_baseline)
     qkv = None
     if rank == 0 and not args.no_qkv and args.config == "llama3-8b-decode":
         qkv = qkv_probe()
@@ -647,6 +753,9 @@ def run_ours(args, world, rank, local):
                 "driver_create_us_mean": round(drv["create_ns_total"] / max(drv["create_calls"], 1) / 1e3, 2),
                 "driver_access_us_mean": round(drv["access_ns_total"] / max(drv["access_calls"], 1) / 1e3, 2),
                 "gpu_stalled_steps": stalls,
+                "gpu_idle_between_steps_ms": round(sum(gaps), 3),
+                "gpu_idle_gap_ms_max": round(max(gaps), 3) if gaps else 0.0,
+                "host_wait_ms_total": round((wl.host_wait_ns - wait_ns0) / 1e6, 3),
                 "chained_steps": chained,
                 "lead_chunks": wl.lead_chunks,
                 "ready_note": ("chained layers leave the driver one plain kernel boundary per "
@@ -654,8 +763,20 @@ def run_ours(args, world, rank, local):
                                "several steps, covered by extending lead_chunks ahead"
                                if wl.chain else "plain launches"),
                 "host_waited_steps": wl.host_waits - waits0,
-                "hidden": stalls == 0,
+                "hidden": stalls == 0 and wl.host_waits - waits0 == 0,
+                "hidden_rule": ("no step waited on the host for a mapping and the GPU never ran "
+                                "dry behind one; compare ms_per_step with the --premap twin"),
+                "driver_threads": drv_end.get("driver_threads"),
+                "phys_reserve_chunks": wl.phys_reserve,
+                "creates_from_reserve": drv["reserve_hits"],
+                "driver_creates": drv["create_calls"],
+                "phys_reserve_note": ("pre-created physical handles (cuMemCreate before the timed "
+                                      "region; the logical create_chunk + cuMemMap/SetAccess of "
+                                      "every extend still happen on demand inside it)"),
             },
+            "check": check,
+            "growth": ({"from_tokens": GROWTH_START, "to_tokens": max(wl.host_lens),
+                        "timed_steps": args.steps} if args.growth else None),
             "gpu_launches": launches + 0,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -670,7 +791,7 @@ def run_ours(args, world, rank, local):
 
 
 # ------------------------------------------------------- config-3 prefill --
-def prefill_probe(iters: int = 8) -> dict:
+def prefill_probe(iters: int = 8, check: bool = False, cpu: bool = True) -> dict:
     """Config 3 through the manager: a 2048-token conversation is recorded in
     the rTree, 16 follow-up turns prefix-match it (128 shared chunks mapped by
     identity + 32 new chunks each), and the tcgen05 prefix-prefill kernel runs
@@ -728,12 +849,66 @@ def prefill_probe(iters: int = 8) -> dict:
     except Exception:
         pk = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
     tf = flops / per / 1e12
+    res = {"workload": "config 3: 16 x (2048 rTree-shared + 512 new), Llama-3-8B heads, per layer",
+           "prefix_shared_by_identity": bool(shared_ok), "us_per_layer": round(per * 1e6, 1),
+           "tflops": round(tf, 1), "frac_of_bf16_burst": round(tf / pk["bf16_tflops"], 4),
+           "frac_of_bf16_sustained": round(tf / pk["bf16_tflops_sustained"], 4),
+           "frac_note": "a ~70 ms probe of back-to-back launches: burst is the denominator",
+           "kernel": "vt::pf::prefill_kernel (tcgen05/TMEM/TMA)", "launches": last_launches()}
+    if check:
+        # the last launch was layer L-1: sampled (request, kv head) slices vs the oracle
+        from oracle.attention_ref import prefill_attention_ref, rel_err
+        from paper_2407_15309_b200.kv_layout import read_kv
+
+        G = hq // hkv
+        rows, worst = [], 0.0
+        for b, h in ((0, 0), (7, 3), (15, 7)):
+            k, v = read_kv(vas[b], prefix + n_new, L - 1, geo)
+            qs = q[b, :, h * G:(h + 1) * G].cpu()
+            ref = prefill_attention_ref(qs, k[h:h + 1].cpu(), v[h:h + 1].cpu(), prefix)
+            err = rel_err(out[b, :, h * G:(h + 1) * G].cpu(), ref)
+            worst = max(worst, err)
+            rows.append({"request": b, "kv_head": h, "rel_err": round(err, 5)})
+        res["check"] = {"samples": rows, "max_rel_err": round(worst, 5), "tol": 2e-2,
+                        "ok": worst <= 2e-2, "batch": B}
+    if cpu:
+        res["cpu_baseline"] = prefill_cpu_baseline(q, vas, geo, prefix, n_new, L - 1)
     dev.wait()
-    return {"workload": "config 3: 16 x (2048 rTree-shared + 512 new), Llama-3-8B heads, per layer",
-            "prefix_shared_by_identity": bool(shared_ok), "us_per_layer": round(per * 1e6, 1),
-            "tflops": round(tf, 1), "frac_of_bf16_sustained": round(tf / pk["bf16_tflops_sustained"], 4),
-            "frac_of_bf16_burst": round(tf / pk["bf16_tflops"], 4),
-            "kernel": "vt::pf::prefill_kernel (tcgen05/TMEM/TMA)", "launches": last_launches()}
+    return res
+
+
+def prefill_cpu_baseline(q, vas, geo, prefix: int, n_new: int, layer: int,
+                         budget_s: float = 6.0) -> dict:
+    """CPU causal prefix-prefill (torch fp32 matmuls on all host threads) over
+    the same KV bytes: one request's 512 new tokens x 32 q heads against its
+    2048 + 512 tokens, repeated for about `budget_s`."""
+    import torch
+
+    from paper_2407_15309_b200.kv_layout import read_kv
+
+    k, v = read_kv(vas[0], prefix + n_new, layer, geo)
+    k, v, qq = k.cpu().float(), v.cpu().float(), q[0].cpu().float()  # [Hkv, L, d], [n, Hq, d]
+    hkv, G = geo.kv_heads, geo.group
+    pos = prefix + torch.arange(n_new)
+    mask = torch.arange(prefix + n_new)[None, :] > pos[:, None]
+    scale = 1.0 / math.sqrt(geo.head_dim)
+
+    def once():
+        qh = qq.permute(1, 0, 2).reshape(hkv, G * n_new, geo.head_dim)
+        sc = torch.matmul(qh, k.transpose(1, 2)).view(hkv, G, n_new, -1) * scale
+        sc.masked_fill_(mask, float("-inf"))
+        return torch.matmul(torch.softmax(sc, dim=-1).view(hkv, G * n_new, -1), v)
+
+    once()
+    t0, reps = time.perf_counter(), 0
+    while time.perf_counter() - t0 < budget_s and reps < 50:
+        once()
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    flops = 4 * geo.q_heads * geo.head_dim * (n_new * prefix + n_new * (n_new + 1) // 2)
+    return {"value": round(flops / dt / 1e12, 4), "unit": "TFLOP/s",
+            "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"1 request x 1 layer ({n_new} new over {prefix} prefix, 32q/8kv), {reps} reps"}
 
 
 # ---------------------------------------------- fused QKV + KV append probe --
@@ -875,6 +1050,9 @@ def manager_cpu_baseline(reference_only: bool = False) -> dict:
     from oracle import vtm_ref as R
 
     arms = [("reference_port", R)]
+    kv = _reference_kvsim()
+    if kv is not None:
+        arms.insert(0, ("reference_kvsim", kv))
     if not reference_only:
         import paper_2407_15309_b200 as vt
 
@@ -926,8 +1104,29 @@ def manager_cpu_baseline(reference_only: bool = False) -> dict:
                      "prefix_record_2048_us_p50": round(rec[len(rec) // 2] / 1e3, 1),
                      "prefix_match_2048_512_us_p50": round(match[len(match) // 2] / 1e3, 1)}
     out["cores"] = 1
-    out["kind"] = "port"
+    out["kind"] = "reference" if kv is not None else "port"
     return out
+
+
+def _reference_kvsim():
+    """The unmodified reference package (kvsim) from baseline/_ref, installed
+    with `pip install --no-index ... --target baseline/_ref` (DESIGN.md §9);
+    None when it is not there."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "kvsim")):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import kvsim
+    except Exception:
+        return None
+    return kvsim
+
+
+def _first(d: dict) -> dict:
+    name = "reference_kvsim" if "reference_kvsim" in d else "reference_port"
+    return dict(d[name], impl=name, kind=d["kind"], cores=1)
 
 
 def run_reference(args, world, rank):
@@ -940,25 +1139,27 @@ def run_reference(args, world, rank):
     from oracle.attention_ref import decode_attention_torch_cpu
 
     gen = torch.Generator().manual_seed(0)
-    nb = min(B, 4)
+    nb = B  # the whole batch of one layer (1 GiB of KV at config 2) per step
     k = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
     v = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
     q = torch.randn(nb, hq, 128, generator=gen).to(torch.bfloat16)
     lens = [ctx] * nb
-    for _ in range(args.warmup):
+    steps, warm = min(args.steps, 10), min(args.warmup, 2)  # bounded: ~0.5 s per step
+    for _ in range(warm):
         decode_attention_torch_cpu(q, k, v, lens)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(steps):
         decode_attention_torch_cpu(q, k, v, lens)
     dt = time.perf_counter() - t0
-    kv_bytes = (2 * nb * hkv * ctx * 128 * 2 + 2 * nb * hq * 128 * 2) * args.steps
+    kv_bytes = (2 * nb * hkv * ctx * 128 * 2 + 2 * nb * hq * 128 * 2) * steps
     value = kv_bytes / dt / 1e9
-    sample = f"{nb} requests x 1 layer x {ctx} tokens per step ({hq}q/{hkv}kv heads)"
+    sample = (f"all {nb} requests x 1 of {L} layers x {ctx} tokens per step ({hq}q/{hkv}kv "
+              f"heads); {steps} timed steps after {warm} warm-up")
     line = {
         "impl": "reference",
         "metric": "decode-attn KV GB/s (% of HBM peak) and tokens/s; vTensor extend latency",
-        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": args.config, "sample": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s",
@@ -966,14 +1167,34 @@ def run_reference(args, world, rank):
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         # the metric's other half: vTensor extend / token append through the
-        # reference's manager algorithm (oracle/vtm_ref.py), 1 host core
-        "extend": manager_cpu_baseline(reference_only=True)["reference_port"],
+        # reference's own manager (kvsim from baseline/_ref; else the port), 1 host core
+        "extend": _first(manager_cpu_baseline(reference_only=True)),
     }
     print(json.dumps(line))
 
 
+def self_launch(n: int) -> None:
+    """`python bench.py --gpus N` without torchrun: re-run this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous), so
+    --gpus N always measures N processes. Exits with the launcher's code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        self_launch(args.gpus)
+    if env_world is not None and int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
     hang_s = float(os.environ.get("VT_BENCH_HANG_DUMP_S", "0"))
     if hang_s > 0:  # diagnostics: dump every thread's stack if the run wedges
         import faulthandler

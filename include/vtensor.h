@@ -91,6 +91,9 @@ typedef struct vt_driver_stats {
   int64_t access_ns_total; /* cuMemSetAccess share of map_ns_total */
   int64_t fence_waits, fence_wait_ns_total;
   int64_t max_op_ns;
+  int64_t reserve_hits;   /* creates served from the pre-created reserve */
+  int64_t reserve_chunks; /* handles in the reserve now */
+  int64_t driver_threads; /* threads executing driver ops in parallel */
 } vt_driver_stats;
 
 /* ---- lifetime ------------------------------------------------------------
@@ -161,6 +164,23 @@ int vt_poll(const vt_device* dev, uint64_t ticket, int* done);
 int vt_fence(vt_device* dev, void* cuda_stream);
 int vt_set_async(vt_device* dev, int enabled);
 int vt_driver_stats_get(const vt_device* dev, vt_driver_stats* out);
+/* Driver-op parallelism (no reference counterpart: the reference's device is
+ * in-process and instantaneous, device.py:118-295). Each queued batch runs
+ * as maximal same-kind segments in issue order; the ops of one segment are
+ * independent and run on `threads` threads (default 4, env VT_DRIVER_THREADS).
+ * On the B200 driver each cuMemCreate / cuMemSetAccess / cuMemUnmap waits
+ * 150-720 us (not CPU-bound), so parallel callers multiply the mapping rate
+ * (tools/vmm_probe.cu). Blocks until queued work has drained. */
+int vt_set_driver_threads(vt_device* dev, int threads);
+/* Physical-handle reserve: keep up to `chunks` cuMemCreate'd handles that are
+ * not (yet) logical chunks. A logical create_chunk takes one from the reserve
+ * instead of calling cuMemCreate on the extend path, and a destroyed chunk's
+ * memory refills it while it is short. Purely physical: the call log, byte
+ * accounting and every manager decision are unchanged (the reserve is HBM the
+ * budget does not see — size it inside the headroom between the configured
+ * capacity and the device). Queues a fill: vt_wait(vt_ticket()) returns once
+ * it is full. 0 releases it. */
+int vt_set_phys_reserve(vt_device* dev, int64_t chunks);
 /* Submit -> completed latency (ns) of every driver op of kind `op` (a vt_op
  * code: create/map/unmap/destroy/release) completed since the last reset;
  * copies up to `cap` samples, *n = total available. reset != 0 clears. This

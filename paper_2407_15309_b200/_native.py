@@ -88,6 +88,9 @@ class VtDriverStats(ctypes.Structure):
         ("fence_waits", c_int64),
         ("fence_wait_ns_total", c_int64),
         ("max_op_ns", c_int64),
+        ("reserve_hits", c_int64),
+        ("reserve_chunks", c_int64),
+        ("driver_threads", c_int64),
     ]
 
 
@@ -142,6 +145,8 @@ def vtensor_lib() -> ctypes.CDLL:
         "vt_poll": (c_int, [c_void_p, c_uint64, POINTER(c_int)]),
         "vt_fence": (c_int, [c_void_p, c_void_p]),
         "vt_set_async": (c_int, [c_void_p, c_int]),
+        "vt_set_driver_threads": (c_int, [c_void_p, c_int]),
+        "vt_set_phys_reserve": (c_int, [c_void_p, c_int64]),
         "vt_driver_stats_get": (c_int, [c_void_p, POINTER(VtDriverStats)]),
         "vt_driver_latencies": (c_int, [c_void_p, c_int32, P64, c_int64, P64, c_int]),
         "vt_va": (c_int, [c_void_p, c_int64, POINTER(c_uint64)]),
@@ -166,6 +171,6 @@ VTENSOR_SYMBOLS = (
     "vt_set_active_requests", "vt_get_stats", "vt_resolve", "vt_handle_alive",
     "vt_live_handles", "vt_live_ranges", "vt_range_mappings",
     "vt_call_log_len", "vt_call_log_read", "vt_ticket", "vt_wait", "vt_poll",
-    "vt_fence", "vt_set_async", "vt_driver_stats_get", "vt_driver_latencies", "vt_va",
+    "vt_fence", "vt_set_async", "vt_set_driver_threads", "vt_set_phys_reserve", "vt_driver_stats_get", "vt_driver_latencies", "vt_va",
     "vt_encode_tensor_map", "vt_dev_set_shareable", "vt_export_chunk", "vt_import_chunk", "vt_chunk_is_imported",
 )

@@ -28,8 +28,10 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <set>
@@ -55,6 +57,7 @@ struct Driver {
   CUresult (*Init)(unsigned int);
   CUresult (*DeviceGet)(CUdevice*, int);
   CUresult (*PrimaryCtxRetain)(CUcontext*, CUdevice);
+  CUresult (*PrimaryCtxRelease)(CUdevice);
   CUresult (*CtxSetCurrent)(CUcontext);
   CUresult (*CtxGetCurrent)(CUcontext*);
   CUresult (*AddrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
@@ -72,6 +75,9 @@ struct Driver {
   CUresult (*EventRecord)(CUevent, CUstream);
   CUresult (*EventSynchronize)(CUevent);
   CUresult (*EventDestroy)(CUevent);
+  CUresult (*StreamCreate)(CUstream*, unsigned int);
+  CUresult (*StreamDestroy)(CUstream);
+  CUresult (*StreamWaitEvent)(CUstream, CUevent, unsigned int);
   CUresult (*GetErrorString)(CUresult, const char**);
   // Optional (cross-device chunk sharing): nullptr if the driver lacks them.
   CUresult (*ExportShareable)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
@@ -107,6 +113,7 @@ Driver& driver() {
     VT_SYM(Init, "cuInit");
     VT_SYM(DeviceGet, "cuDeviceGet");
     VT_SYM(PrimaryCtxRetain, "cuDevicePrimaryCtxRetain");
+    VT_SYM(PrimaryCtxRelease, "cuDevicePrimaryCtxRelease_v2");
     VT_SYM(CtxSetCurrent, "cuCtxSetCurrent");
     VT_SYM(CtxGetCurrent, "cuCtxGetCurrent");
     VT_SYM(AddrReserve, "cuMemAddressReserve");
@@ -121,6 +128,9 @@ Driver& driver() {
     VT_SYM(EventRecord, "cuEventRecord");
     VT_SYM(EventSynchronize, "cuEventSynchronize");
     VT_SYM(EventDestroy, "cuEventDestroy_v2");
+    VT_SYM(StreamCreate, "cuStreamCreate");
+    VT_SYM(StreamDestroy, "cuStreamDestroy_v2");
+    VT_SYM(StreamWaitEvent, "cuStreamWaitEvent");
     VT_SYM(GetErrorString, "cuGetErrorString");
     VT_SYM(TensorMapEncodeTiled, "cuTensorMapEncodeTiled");
 #undef VT_SYM
@@ -146,7 +156,7 @@ std::string cu_err(CUresult r) {
 // ---------------------------------------------------------------------------
 // Worker-side driver ops.
 // ---------------------------------------------------------------------------
-enum class DrvKind : uint8_t { kCreate, kMap, kUnmap, kDestroy, kRelease, kExport, kImport };
+enum class DrvKind : uint8_t { kCreate, kMap, kUnmap, kDestroy, kRelease, kExport, kImport, kFill };
 
 struct DrvOp {
   DrvKind kind;
@@ -158,6 +168,7 @@ struct DrvOp {
   int64_t submit_ns;
   int fd;                // import: the shareable handle (consumed)
   int* fd_out;           // export: where the new shareable handle goes
+  bool imported;         // destroy: the chunk belongs to another pool
 };
 
 constexpr int kFenceRing = 64;
@@ -190,9 +201,10 @@ struct vt_device {
 
   // --- CUDA backend ---
   CUcontext ctx = nullptr;
+  CUdevice cu_dev = 0;
   CUmemAllocationProp prop{};
   CUmemAccessDesc access{};
-  bool async = true;
+  bool async = true;  // guarded by mu (the worker reads it in its wait predicate)
   std::thread worker;
   std::mutex mu;
   std::condition_variable cv_work, cv_done;
@@ -202,20 +214,40 @@ struct vt_device {
   std::atomic<uint64_t> done_ticket{0};     // completed
   std::string drv_error;                    // sticky worker error
   std::atomic<bool> drv_failed{false};
+  // Fences: vt_fence(stream) makes a private in-order fence stream wait on
+  // the caller's stream and records epoch e there, so epoch e completing
+  // implies every earlier fence (whatever stream it named) has completed.
+  CUstream fence_stream = nullptr;
+  CUevent fence_src = nullptr;              // scratch: marks the caller's stream
   CUevent fence_events[kFenceRing] = {};
   uint64_t fence_epoch = 0;                 // recorded by the caller
   uint64_t synced_epoch = 0;                // waited by the worker
-  std::unordered_map<int64_t, CUmemGenericAllocationHandle> phys;  // worker-owned
+  std::mutex phys_mu;  // phys + reserve (pool threads)
+  std::unordered_map<int64_t, CUmemGenericAllocationHandle> phys;
+  std::vector<CUmemGenericAllocationHandle> reserve;  // pre-created, not yet a logical chunk
+  int64_t reserve_target = 0;
+  std::mutex stat_mu;
   vt_driver_stats dstats{};
+  // driver pool (parallel_for); the worker thread is member 0
+  std::vector<std::thread> pool;
+  std::mutex pool_mu;
+  std::condition_variable pool_cv, pool_done_cv;
+  const std::function<void(size_t)>* job_fn = nullptr;
+  size_t job_n = 0;
+  uint64_t job_gen = 0;
+  bool pool_stop = false;
+  std::atomic<size_t> job_next{0}, job_left{0};
+  int driver_threads = 1;
   std::mutex lat_mu;
   std::vector<int64_t> lat[6];  // per vt_op: submit -> completed, ns
 
   bool is_cuda() const { return ordinal >= 0; }
 
   void note_latency(const DrvOp& op, int64_t done_ns) {
+    if (op.kind >= DrvKind::kExport) return;  // not one of the reference's device ops
     static const int kOp[] = {VT_OP_CREATE_CHUNK, VT_OP_MAP_PAGE, VT_OP_UNMAP_PAGE,
                               VT_OP_DESTROY_CHUNK, VT_OP_RELEASE_ADDRESS, VT_OP_CREATE_CHUNK,
-                              VT_OP_CREATE_CHUNK};
+                              VT_OP_CREATE_CHUNK, VT_OP_CREATE_CHUNK};
     std::lock_guard<std::mutex> lk(lat_mu);
     auto& v = lat[kOp[static_cast<int>(op.kind)]];
     if (v.size() < (1u << 20)) v.push_back(done_ns - op.submit_ns);
@@ -273,6 +305,8 @@ struct vt_device {
       cv_work.notify_one();
       return;
     }
+    // Sync mode: the worker is parked (its wait predicate requires `async`),
+    // so the queue is drained here, on the caller's thread, before returning.
     std::vector<DrvOp> batch;
     {
       std::lock_guard<std::mutex> lk(mu);
@@ -281,13 +315,25 @@ struct vt_device {
     }
     if (batch.empty()) return;
     execute_run(batch.data(), batch.size());
-    done_ticket.store(batch.back().ticket);
+  }
+
+  // done_ticket is published under `mu` so a waiter that has checked its
+  // predicate (under `mu`) is already blocked before the notify can happen.
+  void publish_done(uint64_t ticket) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      done_ticket.store(ticket);
+    }
+    cv_done.notify_all();
   }
 
   void record_error(const std::string& what) {
-    std::lock_guard<std::mutex> lk(mu);
-    if (drv_error.empty()) drv_error = what;
-    drv_failed.store(true);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (drv_error.empty()) drv_error = what;
+      drv_failed.store(true);
+    }
+    cv_done.notify_all();
   }
 
   void wait_fence(uint64_t epoch) {
@@ -297,121 +343,284 @@ struct vt_device {
     CUresult r = driver().EventSynchronize(ev);
     if (r != CUDA_SUCCESS) record_error("cuEventSynchronize: " + cu_err(r));
     synced_epoch = epoch;
+    std::lock_guard<std::mutex> lk(stat_mu);
     dstats.fence_waits++;
     dstats.fence_wait_ns_total += now_ns() - t0;
   }
 
-  // Executes ops[0..n) which the caller guarantees are in issue order. A run of
-  // maps onto consecutive pages gets one cuMemSetAccess for the whole run.
+  // ---- physical handle table + reserve (shared by the pool threads) ----
+  CUmemGenericAllocationHandle phys_get(int64_t id, bool* found) {
+    std::lock_guard<std::mutex> lk(phys_mu);
+    auto it = phys.find(id);
+    *found = it != phys.end();
+    return *found ? it->second : 0;
+  }
+  void phys_put(int64_t id, CUmemGenericAllocationHandle h) {
+    std::lock_guard<std::mutex> lk(phys_mu);
+    phys[id] = h;
+  }
+  bool phys_take(int64_t id, CUmemGenericAllocationHandle* h) {
+    std::lock_guard<std::mutex> lk(phys_mu);
+    auto it = phys.find(id);
+    if (it == phys.end()) return false;
+    *h = it->second;
+    phys.erase(it);
+    return true;
+  }
+  // A pre-created handle from the reserve, if any (cuMemCreate off the path).
+  bool reserve_pop(CUmemGenericAllocationHandle* h) {
+    std::lock_guard<std::mutex> lk(phys_mu);
+    if (reserve.empty()) return false;
+    *h = reserve.back();
+    reserve.pop_back();
+    return true;
+  }
+  // A destroyed chunk's memory goes back to the reserve while it is short.
+  bool reserve_push(CUmemGenericAllocationHandle h) {
+    std::lock_guard<std::mutex> lk(phys_mu);
+    if (static_cast<int64_t>(reserve.size()) >= reserve_target) return false;
+    reserve.push_back(h);
+    return true;
+  }
+  int64_t reserve_deficit() {
+    std::lock_guard<std::mutex> lk(phys_mu);
+    return reserve_target - static_cast<int64_t>(reserve.size());
+  }
+
+  void stat_add(int64_t vt_driver_stats::*calls, int64_t vt_driver_stats::*ns, int64_t dt) {
+    std::lock_guard<std::mutex> lk(stat_mu);
+    dstats.*calls += 1;
+    dstats.*ns += dt;
+  }
+
+  // ---- driver thread pool: parallel_for over independent driver ops ----
+  // Measured on the B200 box (tools/vmm_probe.cu "alternate"): one thread
+  // completes 0.5-1.6 map+SetAccess per ms (each call waits 150-720 us on the
+  // driver, not the CPU), four threads 2-6 per ms, and none of it slows the
+  // HBM-streaming kernels running meanwhile.
+  void parallel_for(size_t n, const std::function<void(size_t)>& fn) {
+    if (n == 0) return;
+    if (n == 1 || pool.empty()) {
+      for (size_t k = 0; k < n; ++k) fn(k);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(pool_mu);
+      job_fn = &fn;
+      job_n = n;
+      job_next.store(0);
+      job_left.store(n);
+      ++job_gen;
+    }
+    pool_cv.notify_all();
+    run_job_items(fn, n);
+    std::unique_lock<std::mutex> lk(pool_mu);
+    pool_done_cv.wait(lk, [&] { return job_left.load() == 0; });
+    job_fn = nullptr;
+  }
+  void run_job_items(const std::function<void(size_t)>& fn, size_t n) {
+    for (;;) {
+      size_t k = job_next.fetch_add(1);
+      if (k >= n) return;
+      fn(k);
+      if (job_left.fetch_sub(1) == 1) {
+        std::lock_guard<std::mutex> lk(pool_mu);
+        pool_done_cv.notify_all();
+      }
+    }
+  }
+  void pool_main() {
+    driver().CtxSetCurrent(ctx);
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(size_t)>* fn;
+      size_t n;
+      {
+        std::unique_lock<std::mutex> lk(pool_mu);
+        pool_cv.wait(lk, [&] { return pool_stop || (job_gen != seen && job_fn); });
+        if (pool_stop) return;
+        seen = job_gen;
+        fn = job_fn;
+        n = job_n;
+      }
+      run_job_items(*fn, n);
+    }
+  }
+  void start_pool(int threads) {
+    for (int t = 1; t < threads; ++t) pool.emplace_back([this] { pool_main(); });
+  }
+  void stop_pool() {
+    {
+      std::lock_guard<std::mutex> lk(pool_mu);
+      pool_stop = true;
+    }
+    pool_cv.notify_all();
+    for (auto& t : pool) t.join();
+    pool.clear();
+    pool_stop = false;
+  }
+
+  void do_create(const DrvOp& op) {
+    int64_t t0 = now_ns();
+    CUmemGenericAllocationHandle h = 0;
+    if (reserve_pop(&h)) {
+      phys_put(op.handle_id, h);
+      std::lock_guard<std::mutex> lk(stat_mu);
+      dstats.reserve_hits++;
+      return;
+    }
+    CUresult r = driver().MemCreate(&h, static_cast<size_t>(cfg.chunk_bytes), &prop, 0);
+    if (r != CUDA_SUCCESS)
+      record_error("cuMemCreate: " + cu_err(r));
+    else
+      phys_put(op.handle_id, h);
+    stat_add(&vt_driver_stats::create_calls, &vt_driver_stats::create_ns_total, now_ns() - t0);
+  }
+  void do_map_one(const DrvOp& op) {
+    Driver& d = driver();
+    int64_t t0 = now_ns();
+    bool found = false;
+    CUmemGenericAllocationHandle h = phys_get(op.handle_id, &found);
+    if (!found) {
+      record_error("map of a chunk the driver never created (id " +
+                   std::to_string(op.handle_id) + ")");
+      return;
+    }
+    const size_t len = static_cast<size_t>(cfg.chunk_bytes);
+    CUresult r = d.MemMap(op.addr, len, 0, h, 0);
+    if (r != CUDA_SUCCESS) record_error("cuMemMap: " + cu_err(r));
+    int64_t ta = now_ns();
+    r = d.MemSetAccess(op.addr, len, &access, 1);
+    if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
+    int64_t t1 = now_ns();
+    std::lock_guard<std::mutex> lk(stat_mu);
+    dstats.map_calls++;
+    dstats.access_calls++;
+    dstats.access_ns_total += t1 - ta;
+    dstats.map_ns_total += t1 - t0;
+  }
+  void do_unmap(const DrvOp& op) {
+    int64_t t0 = now_ns();
+    CUresult r = driver().MemUnmap(op.addr, static_cast<size_t>(cfg.chunk_bytes));
+    if (r != CUDA_SUCCESS) record_error("cuMemUnmap: " + cu_err(r));
+    stat_add(&vt_driver_stats::unmap_calls, &vt_driver_stats::unmap_ns_total, now_ns() - t0);
+  }
+  void do_destroy(const DrvOp& op) {
+    int64_t t0 = now_ns();
+    CUmemGenericAllocationHandle h;
+    if (phys_take(op.handle_id, &h)) {
+      // Imported chunks belong to another pool: always drop the reference.
+      if (!op.imported && reserve_push(h)) return;
+      CUresult r = driver().MemRelease(h);
+      if (r != CUDA_SUCCESS) record_error("cuMemRelease: " + cu_err(r));
+    }
+    stat_add(&vt_driver_stats::destroy_calls, &vt_driver_stats::destroy_ns_total, now_ns() - t0);
+  }
+  void fill_reserve() {
+    int64_t n = reserve_deficit();
+    if (n <= 0) return;
+    parallel_for(static_cast<size_t>(n), [&](size_t) {
+      CUmemGenericAllocationHandle h = 0;
+      int64_t t0 = now_ns();
+      CUresult r = driver().MemCreate(&h, static_cast<size_t>(cfg.chunk_bytes), &prop, 0);
+      if (r != CUDA_SUCCESS) {
+        record_error("cuMemCreate (reserve): " + cu_err(r));
+        return;
+      }
+      if (!reserve_push(h)) driver().MemRelease(h);
+      stat_add(&vt_driver_stats::create_calls, &vt_driver_stats::create_ns_total, now_ns() - t0);
+    });
+  }
+  void drain_reserve() {
+    std::vector<CUmemGenericAllocationHandle> hs;
+    {
+      std::lock_guard<std::mutex> lk(phys_mu);
+      hs.swap(reserve);
+    }
+    for (auto h : hs) driver().MemRelease(h);
+  }
+
+  // Executes ops[0..n), in issue order, as maximal segments of one kind. Ops
+  // inside a segment are independent — creates of distinct ids, maps into
+  // distinct free slots of handles created in an earlier segment, unmaps of
+  // distinct mapped slots, releases of handles whose unmaps came earlier — so
+  // each segment runs on the driver pool in parallel; the segment boundary
+  // keeps every cross-kind dependency (create -> map -> unmap -> destroy). A
+  // teardown segment first waits for the newest fence any of its ops names
+  // (epochs are monotone in issue order and the fence stream is in order).
+  // done_ticket advances after every segment, so maps are ready before a
+  // later fenced unmap in the same batch has waited for its kernels.
   void execute_run(DrvOp* ops, size_t n) {
     Driver& d = driver();
     size_t i = 0;
     while (i < n) {
-      DrvOp& op = ops[i];
-      int64_t t0 = now_ns();
-      switch (op.kind) {
-        case DrvKind::kCreate: {
-          CUmemGenericAllocationHandle h = 0;
-          CUresult r = d.MemCreate(&h, static_cast<size_t>(cfg.chunk_bytes), &prop, 0);
-          if (r != CUDA_SUCCESS) {
-            record_error("cuMemCreate: " + cu_err(r));
-          } else {
-            phys[op.handle_id] = h;
-          }
-          dstats.create_calls++;
-          dstats.create_ns_total += now_ns() - t0;
-          ++i;
+      const DrvKind kind = ops[i].kind;
+      size_t j = i + 1;
+      const bool parallel = kind == DrvKind::kCreate || kind == DrvKind::kMap ||
+                            kind == DrvKind::kUnmap || kind == DrvKind::kDestroy;
+      if (parallel)
+        while (j < n && ops[j].kind == kind) ++j;
+      DrvOp* seg = ops + i;
+      const size_t m = j - i;
+      if (kind == DrvKind::kUnmap || kind == DrvKind::kDestroy || kind == DrvKind::kRelease)
+        wait_fence(seg[m - 1].fence_epoch);
+      switch (kind) {
+        case DrvKind::kCreate:
+          parallel_for(m, [&](size_t k) { do_create(seg[k]); });
           break;
-        }
-        case DrvKind::kMap: {
-          size_t j = i;
-          CUdeviceptr run_start = op.addr;
-          size_t run_len = 0;
-          while (j < n && ops[j].kind == DrvKind::kMap &&
-                 ops[j].addr == run_start + run_len) {
-            auto it = phys.find(ops[j].handle_id);
-            if (it == phys.end()) {
-              record_error("map of a chunk the driver never created (id " +
-                           std::to_string(ops[j].handle_id) + ")");
-            } else {
-              CUresult r = d.MemMap(ops[j].addr, static_cast<size_t>(cfg.chunk_bytes), 0,
-                                    it->second, 0);
-              if (r != CUDA_SUCCESS) record_error("cuMemMap: " + cu_err(r));
-            }
-            dstats.map_calls++;
-            run_len += static_cast<size_t>(cfg.chunk_bytes);
-            ++j;
-          }
-          int64_t ta = now_ns();
-          CUresult r = d.MemSetAccess(run_start, run_len, &access, 1);
-          if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
-          dstats.access_calls++;
-          dstats.access_ns_total += now_ns() - ta;
-          dstats.map_ns_total += now_ns() - t0;
-          i = j;
+        case DrvKind::kMap:
+          parallel_for(m, [&](size_t k) { do_map_one(seg[k]); });
           break;
-        }
-        case DrvKind::kUnmap: {
-          wait_fence(op.fence_epoch);
-          CUresult r = d.MemUnmap(op.addr, static_cast<size_t>(cfg.chunk_bytes));
-          if (r != CUDA_SUCCESS) record_error("cuMemUnmap: " + cu_err(r));
-          dstats.unmap_calls++;
-          dstats.unmap_ns_total += now_ns() - t0;
-          ++i;
+        case DrvKind::kUnmap:
+          parallel_for(m, [&](size_t k) { do_unmap(seg[k]); });
           break;
-        }
-        case DrvKind::kDestroy: {
-          wait_fence(op.fence_epoch);
-          auto it = phys.find(op.handle_id);
-          if (it != phys.end()) {
-            CUresult r = d.MemRelease(it->second);
-            if (r != CUDA_SUCCESS) record_error("cuMemRelease: " + cu_err(r));
-            phys.erase(it);
-          }
-          dstats.destroy_calls++;
-          dstats.destroy_ns_total += now_ns() - t0;
-          ++i;
+        case DrvKind::kDestroy:
+          parallel_for(m, [&](size_t k) { do_destroy(seg[k]); });
           break;
-        }
         case DrvKind::kRelease: {
-          wait_fence(op.fence_epoch);
-          CUresult r = d.AddrFree(op.addr, op.size);
+          CUresult r = d.AddrFree(seg[0].addr, seg[0].size);
           if (r != CUDA_SUCCESS) record_error("cuMemAddressFree: " + cu_err(r));
-          ++i;
           break;
         }
         case DrvKind::kExport: {
-          auto it = phys.find(op.handle_id);
-          if (it == phys.end()) {
+          bool found = false;
+          CUmemGenericAllocationHandle h = phys_get(seg[0].handle_id, &found);
+          if (!found) {
             record_error("export of a chunk the driver never created (id " +
-                         std::to_string(op.handle_id) + ")");
+                         std::to_string(seg[0].handle_id) + ")");
           } else {
-            CUresult r = d.ExportShareable(op.fd_out, it->second,
+            CUresult r = d.ExportShareable(seg[0].fd_out, h,
                                            CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
             if (r != CUDA_SUCCESS) record_error("cuMemExportToShareableHandle: " + cu_err(r));
           }
-          ++i;
           break;
         }
         case DrvKind::kImport: {
           CUmemGenericAllocationHandle h = 0;
-          CUresult r = d.ImportShareable(&h, reinterpret_cast<void*>(static_cast<intptr_t>(op.fd)),
-                                         CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+          CUresult r = d.ImportShareable(
+              &h, reinterpret_cast<void*>(static_cast<intptr_t>(seg[0].fd)),
+              CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
           if (r != CUDA_SUCCESS)
             record_error("cuMemImportFromShareableHandle: " + cu_err(r));
           else
-            phys[op.handle_id] = h;
-          ::close(op.fd);
-          ++i;
+            phys_put(seg[0].handle_id, h);
+          ::close(seg[0].fd);
           break;
         }
+        case DrvKind::kFill:
+          fill_reserve();
+          break;
       }
+      const int64_t done = now_ns();
+      for (size_t k = 0; k < m; ++k) note_latency(seg[k], done);
+      {
+        std::lock_guard<std::mutex> lk(stat_mu);
+        dstats.max_op_ns = std::max<int64_t>(dstats.max_op_ns, done - seg[m - 1].submit_ns);
+        dstats.ops_completed += static_cast<int64_t>(m);
+      }
+      publish_done(seg[m - 1].ticket);
+      i = j;
     }
-    const int64_t done = now_ns();
-    for (size_t k = 0; k < n; ++k) note_latency(ops[k], done);
-    int64_t lat = done - ops[n - 1].submit_ns;
-    dstats.max_op_ns = std::max<int64_t>(dstats.max_op_ns, lat);
-    dstats.ops_completed += static_cast<int64_t>(n);
   }
 
   void worker_main() {
@@ -420,14 +629,12 @@ struct vt_device {
     for (;;) {
       {
         std::unique_lock<std::mutex> lk(mu);
-        cv_work.wait(lk, [&] { return stopping || !queue.empty(); });
-        if (queue.empty() && stopping) return;
+        cv_work.wait(lk, [&] { return stopping || (async && !queue.empty()); });
+        if (stopping && (queue.empty() || !async)) return;
         batch.assign(queue.begin(), queue.end());
         queue.clear();
       }
       execute_run(batch.data(), batch.size());
-      done_ticket.store(batch.back().ticket);
-      cv_done.notify_all();
     }
   }
 };
@@ -525,6 +732,16 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
       delete d;
       return VT_E_CUDA;
     }
+    d->cu_dev = dev;
+    auto fail_open = [&](int code) {
+      for (auto& ev : d->fence_events)
+        if (ev) drv.EventDestroy(ev);
+      if (d->fence_src) drv.EventDestroy(d->fence_src);
+      if (d->fence_stream) drv.StreamDestroy(d->fence_stream);
+      drv.PrimaryCtxRelease(dev);
+      delete d;
+      return code;
+    };
     d->ensure_ctx();
     d->prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     d->prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -534,18 +751,21 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
     if (r != CUDA_SUCCESS || gran == 0 || cfg->chunk_bytes % static_cast<int64_t>(gran) != 0) {
       std::fprintf(stderr, "vtensor: chunk %lld is not a multiple of VMM granularity %zu\n",
                    static_cast<long long>(cfg->chunk_bytes), gran);
-      delete d;
-      return VT_E_ARG;
+      return fail_open(VT_E_ARG);
     }
     d->access.location = d->prop.location;
     d->access.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
     for (auto& ev : d->fence_events) {
       r = drv.EventCreate(&ev, CU_EVENT_DISABLE_TIMING);
-      if (r != CUDA_SUCCESS) {
-        delete d;
-        return VT_E_CUDA;
-      }
+      if (r != CUDA_SUCCESS) return fail_open(VT_E_CUDA);
     }
+    if (drv.EventCreate(&d->fence_src, CU_EVENT_DISABLE_TIMING) != CUDA_SUCCESS ||
+        drv.StreamCreate(&d->fence_stream, CU_STREAM_NON_BLOCKING) != CUDA_SUCCESS)
+      return fail_open(VT_E_CUDA);
+    int threads = 4;
+    if (const char* e = std::getenv("VT_DRIVER_THREADS")) threads = std::atoi(e);
+    d->driver_threads = std::max(1, std::min(threads, 16));
+    d->start_pool(d->driver_threads);
     d->worker = std::thread([d] { d->worker_main(); });
   }
   *out = d;
@@ -561,8 +781,10 @@ int vt_dev_close(vt_device* d) {
     }
     d->cv_work.notify_all();
     if (d->worker.joinable()) d->worker.join();
+    d->stop_pool();
     Driver& drv = driver();
     d->ensure_ctx();
+    d->drain_reserve();
     // Tear down whatever the manager left behind (caller is responsible for
     // having synchronised the streams that read these pages).
     for (auto& kv : d->ranges) {
@@ -576,6 +798,9 @@ int vt_dev_close(vt_device* d) {
     for (auto& kv : d->phys) drv.MemRelease(kv.second);
     for (auto& ev : d->fence_events)
       if (ev) drv.EventDestroy(ev);
+    if (d->fence_src) drv.EventDestroy(d->fence_src);
+    if (d->fence_stream) drv.StreamDestroy(d->fence_stream);
+    drv.PrimaryCtxRelease(d->cu_dev);
   }
   delete d;
   return VT_OK;
@@ -709,11 +934,13 @@ int vt_destroy_chunk(vt_device* d, int64_t id) {
   d->handles.erase(it);
   // An imported chunk's release drops this device's reference only; it is not
   // one of the reference's device ops, so it stays out of the call log.
-  if (d->imported.erase(id) == 0) d->log_call(VT_OP_DESTROY_CHUNK, 0, 0, id, 0);
+  const bool imported = d->imported.erase(id) != 0;
+  if (!imported) d->log_call(VT_OP_DESTROY_CHUNK, 0, 0, id, 0);
   if (d->is_cuda()) {
     DrvOp op{};
     op.kind = DrvKind::kDestroy;
     op.handle_id = id;
+    op.imported = imported;
     d->enqueue(op);
     d->kick();
   }
@@ -729,6 +956,7 @@ int vt_dev_set_shareable(vt_device* d, int enabled) {
   // executes a create; ops already queued keep the old setting only if they
   // ran before this call, so drain first).
   vt_wait(d, vt_ticket(d));
+  d->drain_reserve();  // pre-created handles carry the old allocation properties
   d->prop.requestedHandleTypes =
       enabled ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR : CU_MEM_HANDLE_TYPE_NONE;
   return VT_OK;
@@ -904,11 +1132,17 @@ int vt_poll(const vt_device* d, uint64_t ticket, int* done) {
 int vt_fence(vt_device* d, void* stream) {
   if (!d->is_cuda()) return VT_OK;
   d->ensure_ctx();
-  // Worker may still need the slot we are about to overwrite; re-recording is
-  // safe (the later event completes no earlier than the old one).
+  Driver& drv = driver();
+  // Route every fence through the one in-order fence stream: epoch e then
+  // completes only after all earlier fences, whichever streams they named, so
+  // a teardown op that waits for its own epoch also waits for every kernel
+  // fenced before it. The worker may still wait on the ring slot being
+  // re-recorded; that is safe because the later record completes no earlier.
+  CUresult r = drv.EventRecord(d->fence_src, reinterpret_cast<CUstream>(stream));
+  if (r == CUDA_SUCCESS) r = drv.StreamWaitEvent(d->fence_stream, d->fence_src, 0);
+  if (r != CUDA_SUCCESS) return d->fail(VT_E_CUDA, "fence: " + cu_err(r));
   uint64_t e = d->fence_epoch + 1;
-  CUresult r = driver().EventRecord(d->fence_events[e % kFenceRing],
-                                    reinterpret_cast<CUstream>(stream));
+  r = drv.EventRecord(d->fence_events[e % kFenceRing], d->fence_stream);
   if (r != CUDA_SUCCESS) return d->fail(VT_E_CUDA, "cuEventRecord: " + cu_err(r));
   std::lock_guard<std::mutex> lk(d->mu);
   d->fence_epoch = e;
@@ -918,12 +1152,52 @@ int vt_fence(vt_device* d, void* stream) {
 int vt_set_async(vt_device* d, int enabled) {
   if (!d->is_cuda()) return VT_OK;
   if (!enabled) vt_wait(d, vt_ticket(d));  // drain before switching to inline
-  d->async = enabled != 0;
+  {
+    std::lock_guard<std::mutex> lk(d->mu);
+    d->async = enabled != 0;
+  }
+  d->cv_work.notify_one();
   return VT_OK;
 }
 
 int vt_driver_stats_get(const vt_device* d, vt_driver_stats* out) {
-  *out = d->dstats;
+  auto* md = const_cast<vt_device*>(d);
+  {
+    std::lock_guard<std::mutex> lk(md->stat_mu);
+    *out = d->dstats;
+  }
+  std::lock_guard<std::mutex> lk(md->phys_mu);
+  out->reserve_chunks = static_cast<int64_t>(d->reserve.size());
+  out->driver_threads = d->driver_threads;
+  return VT_OK;
+}
+
+int vt_set_driver_threads(vt_device* d, int threads) {
+  if (threads < 1 || threads > 16) return d->fail(VT_E_ARG, "driver threads must be in 1..16");
+  if (!d->is_cuda()) return VT_OK;
+  vt_wait(d, vt_ticket(d));  // the pool is idle between batches once drained
+  std::lock_guard<std::mutex> lk(d->mu);  // keeps the worker from starting a batch
+  d->stop_pool();
+  d->driver_threads = threads;
+  d->start_pool(threads);
+  return VT_OK;
+}
+
+int vt_set_phys_reserve(vt_device* d, int64_t chunks) {
+  if (chunks < 0) return d->fail(VT_E_ARG, "reserve size cannot be negative");
+  if (!d->is_cuda()) return VT_OK;
+  {
+    std::lock_guard<std::mutex> lk(d->phys_mu);
+    d->reserve_target = chunks;
+    while (static_cast<int64_t>(d->reserve.size()) > chunks) {
+      driver().MemRelease(d->reserve.back());
+      d->reserve.pop_back();
+    }
+  }
+  DrvOp op{};
+  op.kind = DrvKind::kFill;
+  d->enqueue(op);
+  d->kick();
   return VT_OK;
 }
 

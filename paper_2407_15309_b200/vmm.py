@@ -480,6 +480,20 @@ class VirtualMemoryDevice:
     def set_async(self, enabled: bool) -> None:
         self._lib.vt_set_async(self._h, int(bool(enabled)))
 
+    def set_driver_threads(self, threads: int) -> None:
+        """Threads executing independent driver ops of a batch in parallel."""
+        rc = self._lib.vt_set_driver_threads(self._h, int(threads))
+        if rc:
+            self._raise(rc)
+
+    def set_phys_reserve(self, chunks: int) -> None:
+        """Keep up to `chunks` pre-created physical handles (cuMemCreate off
+        the extend path); purely physical, invisible to the call log and the
+        byte budget. ``wait()`` returns once the reserve is full."""
+        rc = self._lib.vt_set_phys_reserve(self._h, int(chunks))
+        if rc:
+            self._raise(rc)
+
     def driver_latencies(self, op: str = "map_page", reset: bool = False) -> list[int]:
         """Submit->completed latency (ns) of the driver ops of one kind."""
         code = N.OP_NAMES.index(op)
