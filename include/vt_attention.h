@@ -105,6 +105,22 @@ int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
                          const void* kv_maps, const int32_t* start, int32_t batch,
                          int32_t n_new, float scale, void* out, void* stream);
 
+/* Variable-length prefill of the requests one engine step admits (the engine
+ * charges sum(len - shared) prefill tokens, kvsim/engine.py:422-484, 500-504):
+ * request b has n_b = q_offsets[b+1] - q_offsets[b] new tokens at positions
+ * [start_b, start_b + n_b), one launch for the whole batch.
+ *   q, out    : packed [total_tokens, q_heads, head_dim] bf16, request b's rows
+ *               at [q_offsets[b], q_offsets[b+1])
+ *   q_offsets : [batch + 1] i32 device, q_offsets[0] = 0, non-decreasing,
+ *               q_offsets[batch] = total_tokens (cu_seqlens convention)
+ *   max_n_new : host upper bound of n_b (sizes the tile grid)
+ *   kv_maps   : chunk extent >= start_b + n_b;  start : [batch] i32 device
+ * Same errors as vt_prefill_attention; q_offsets == NULL is an error. */
+int vt_prefill_attention_varlen(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                const void* kv_maps, const int32_t* start,
+                                const int32_t* q_offsets, int32_t batch, int32_t max_n_new,
+                                int64_t total_tokens, float scale, void* out, void* stream);
+
 /* Fused QKV projection + KV append, tcgen05; each
  * 128-feature tile's K halves run on a 2-CTA cluster and are reduced through
  * distributed shared memory (no global workspace):

@@ -53,6 +53,9 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_prefill_attention.argtypes = [POINTER(_Geo), c_int32, P, P, P, c_int32, c_int32,
                                              c_float, P, P]
         lib.vt_prefill_attention.restype = c_int
+        lib.vt_prefill_attention_varlen.argtypes = [POINTER(_Geo), c_int32, P, P, P, P, c_int32,
+                                                    c_int32, c_int64, c_float, P, P]
+        lib.vt_prefill_attention_varlen.restype = c_int
         lib.vt_kv_tensor_maps.argtypes = [POINTER(_Geo), P, P, c_int32, P]
         lib.vt_kv_tensor_maps.restype = c_int
         lib.vt_qkv_append.argtypes = [POINTER(_Geo), c_int32, P, P, c_int32, c_int32, P, P, P, P,
@@ -68,7 +71,8 @@ def attn_lib() -> ctypes.CDLL:
 
 ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_chained", "vt_decode_attention_paged",
                 "vt_decode_workspace_bytes", "vt_kv_append",
-                "vt_kv_tensor_maps", "vt_prefill_attention", "vt_qkv_append",
+                "vt_kv_tensor_maps", "vt_prefill_attention", "vt_prefill_attention_varlen",
+                "vt_qkv_append",
                 "vt_qkv_pack_weight",
                 "vt_attn_last_launches")
 
@@ -323,6 +327,33 @@ def prefill_attention(q: torch.Tensor, kv_maps: torch.Tensor, start: torch.Tenso
                                          kv_maps.data_ptr(), start.data_ptr(), B, n_new, scale,
                                          out.data_ptr(), _stream(stream))
     _check(rc, "vt_prefill_attention")
+    return out
+
+
+def prefill_attention_varlen(q: torch.Tensor, kv_maps: torch.Tensor, start: torch.Tensor,
+                             q_offsets: torch.Tensor, max_n_new: int, layer: int, geo: KVGeometry,
+                             out: torch.Tensor | None = None, scale: float | None = None,
+                             stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Variable-length prefill in one launch: q packed ``[T, Hq, d]``, request
+    b's ``n_b = q_offsets[b+1] - q_offsets[b]`` new tokens (rows
+    ``[q_offsets[b], q_offsets[b+1])``) sit at positions
+    ``[start_b, start_b + n_b)`` and attend causally to the cache. ``kv_maps``
+    chunk extent must cover ``start_b + n_b``; ``max_n_new`` >= every n_b."""
+    T = q.shape[0]
+    B = start.shape[0]
+    if q.dtype != torch.bfloat16 or q.shape[1:] != (geo.q_heads, geo.head_dim):
+        raise ValueError(f"q must be bf16 [T, {geo.q_heads}, {geo.head_dim}]")
+    if q_offsets.dtype != torch.int32 or q_offsets.shape != (B + 1,):
+        raise ValueError("q_offsets must be int32 [batch + 1]")
+    if out is None:
+        out = torch.empty_like(q)
+    _need_cuda(q, kv_maps, start, q_offsets, out)
+    if scale is None:
+        scale = 1.0 / math.sqrt(geo.head_dim)
+    rc = attn_lib().vt_prefill_attention_varlen(
+        ctypes.byref(_geo(geo)), layer, q.data_ptr(), kv_maps.data_ptr(), start.data_ptr(),
+        q_offsets.data_ptr(), B, max_n_new, T, scale, out.data_ptr(), _stream(stream))
+    _check(rc, "vt_prefill_attention_varlen")
     return out
 
 

@@ -156,10 +156,11 @@ __device__ long long g_pf_sub[256][4];  // slot 0 row 0: ld done, max done, exp 
 #endif
 
 struct Args {
-  __nv_bfloat16* out;       // [B, n_new, Hq, D]
+  __nv_bfloat16* out;       // [total, Hq, D]: request b's rows at [q_off[b], q_off[b+1])
   const CUtensorMap* kv;    // [B] per-request maps
   const int32_t* start;     // [B]
-  int32_t n_new, hq, hkv, tpc, layer, slots;
+  const int32_t* q_off;     // [B+1] token offsets (varlen), or null: uniform n_new
+  int32_t n_new, hq, hkv, tpc, layer, slots;  // n_new: max new tokens of any request
   int32_t batch, pairs, n_qtiles, n_items;
   float scale_log2;
 };
@@ -167,8 +168,11 @@ struct Args {
 // Work item w -> (q tile, head pair, request). Longest q tiles first (a
 // tile's key count grows with t), pairs of one kv head adjacent so concurrent
 // CTAs share K/V tiles in L2; CTAs take items w = blockIdx.x + k * gridDim.x.
+// With variable-length requests the tile grid is sized by the longest one;
+// tiles past a shorter request's n_b are empty items every role skips.
 struct Item {
-  int t, h0, b, start, kv_len, n_kv, blk_k, blk_v;
+  int t, h0, b, start, kv_len, n_kv, blk_k, blk_v, q0, n_b;
+  bool valid;
 };
 __device__ __forceinline__ Item item_of(int w, const Args& a) {
   Item it;
@@ -178,8 +182,16 @@ __device__ __forceinline__ Item item_of(int w, const Args& a) {
   it.h0 = (r % a.pairs) * a.slots;
   it.b = r / a.pairs;
   it.start = a.start[it.b];
-  it.kv_len = it.start + a.n_new;
-  const int q_last = min(a.n_new, (it.t + 1) * BM);  // exclusive, relative to start
+  if (a.q_off) {
+    it.q0 = a.q_off[it.b];
+    it.n_b = a.q_off[it.b + 1] - it.q0;
+  } else {
+    it.q0 = it.b * a.n_new;
+    it.n_b = a.n_new;
+  }
+  it.valid = it.t * BM < it.n_b;
+  it.kv_len = it.start + it.n_b;
+  const int q_last = min(it.n_b, (it.t + 1) * BM);  // exclusive, relative to start
   it.n_kv = (it.start + q_last + BN - 1) / BN;
   const int hk = it.h0 / (a.hq / a.hkv);
   it.blk_k = (a.layer * 2 + 0) * a.hkv + hk;
@@ -232,25 +244,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t once = l2_evict_first_policy();
         int g = 0;  // K/V tiles loaded so far
         int n = 0;  // items so far
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++n) {
+        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
           const Item it = item_of(w, a);
+          if (!it.valid) continue;
           const CUtensorMap* kvmap = a.kv + it.b;
           if (n >= 1) mbar_wait(&sm.q_empty, (n - 1) & 1);  // last S of the previous item done
           mbar_arrive_expect_tx(&sm.q_full, nslots * 2 * BM * 64 * 2);
           for (int s = 0; s < nslots; ++s) {
-            tma_load_4d(sm.q[s][0], &q_map, &sm.q_full, 0, it.h0 + s, it.t * BM, it.b, once);
-            tma_load_4d(sm.q[s][1], &q_map, &sm.q_full, 64, it.h0 + s, it.t * BM, it.b, once);
+            tma_load_4d(sm.q[s][0], &q_map, &sm.q_full, 0, it.h0 + s, it.q0 + it.t * BM, 0, once);
+            tma_load_4d(sm.q[s][1], &q_map, &sm.q_full, 64, it.h0 + s, it.q0 + it.t * BM, 0, once);
           }
           // The next item's Q and first K/V tiles cannot enter shared memory
           // until this item's last tiles leave it; warm L2 with them now so
           // those loads are L2 hits at the item boundary instead of HBM trips
           // (measured: the tensor pipe idled ~6000 clk per item boundary).
-          if (w + static_cast<int>(gridDim.x) < a.n_items) {
-            const Item nx = item_of(w + gridDim.x, a);
+          const Item nx = w + static_cast<int>(gridDim.x) < a.n_items ? item_of(w + gridDim.x, a)
+                                                                     : Item{};
+          if (nx.valid) {
             for (int s = 0; s < nslots; ++s) {  // its Q tiles too (loaded only after
               // this item's last S, otherwise straight from HBM at the boundary)
-              tma_prefetch_l2_4d(&q_map, 0, nx.h0 + s, nx.t * BM, nx.b);
-              tma_prefetch_l2_4d(&q_map, 64, nx.h0 + s, nx.t * BM, nx.b);
+              tma_prefetch_l2_4d(&q_map, 0, nx.h0 + s, nx.q0 + nx.t * BM, 0);
+              tma_prefetch_l2_4d(&q_map, 64, nx.h0 + s, nx.q0 + nx.t * BM, 0);
             }
             const CUtensorMap* nmap = a.kv + nx.b;
             for (int j = 0; j < min(nx.n_kv, kStages); ++j) {
@@ -276,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_4d(sm.v[st][0], kvmap, &sm.v_full[st], 0, c1, it.blk_v, c3, keep);
             tma_load_4d(sm.v[st][1], kvmap, &sm.v_full[st], 64, c1, it.blk_v, c3, keep);
           }
+          ++n;
         }
       }
       __syncwarp();
@@ -316,8 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::commit(&sm.o_done[s]);
       };
       int g = 0, n = 0;
-      for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++n) {
-        const int n_kv = item_of(w, a).n_kv;
+      for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
+        const Item it = item_of(w, a);
+        if (!it.valid) continue;
+        const int n_kv = it.n_kv;
         // S(0) of every slot; its S buffer was last read by the previous
         // item's final PV, issued before (in-order).
         wait_fence(&sm.q_full, n & 1);
@@ -355,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        ++n;
       }
     }
   } else {
@@ -371,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = 0;  // key blocks processed so far (barrier phases)
       for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
         const Item it = item_of(w, a);
+        if (!it.valid) continue;
         const int qpos = it.start + it.t * BM + row;  // absolute position of this query row
         const int qmin = it.start + it.t * BM;        // smallest query position of the tile
         float m_run = -INFINITY, l_run = 0.f;
@@ -484,12 +503,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tok = it.t * BM + row;
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
         __nv_bfloat16* dst =
-            a.out + ((static_cast<int64_t>(it.b) * a.n_new + tok) * a.hq + (it.h0 + s)) * D;
+            a.out + ((static_cast<int64_t>(it.q0) + tok) * a.hq + (it.h0 + s)) * D;
         uint32_t r[D];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(o_addr + 32 * c, r + 32 * c);
         tc::wait_ld();
-        if (tok < a.n_new) {
+        if (tok < it.n_b) {
           // 32-byte stores (st.global.v8): a thread writes its 256-byte row
           // in 8 instructions instead of 16 — the row-per-thread pattern
           // makes every instruction touch 32 rows 8 KiB apart (epilogue
@@ -532,17 +551,23 @@ extern "C" int vt_prefill_trace(long long* out) {  // 256 x 8 + 256 x 4 values
 }
 #endif
 
-extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
-                                    const void* kv_maps, const int32_t* start, int32_t batch,
-                                    int32_t n_new, float scale, void* out, void* stream) {
+namespace {
+
+int launch_prefill(const vt_kv_geometry* g, int32_t layer, const void* q, const void* kv_maps,
+                   const int32_t* start, const int32_t* q_off, int32_t batch, int32_t max_n_new,
+                   int64_t total, float scale, void* out, void* stream) {
   if (g->head_dim != D || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
-  if (batch <= 0 || n_new <= 0) return 0;
+  if (batch <= 0 || max_n_new <= 0 || total <= 0) return 0;
+  // Q as one packed [total tokens][Hq][D] tensor (a 4-D map with a unit outer
+  // dim): request b's tile t starts at row q_off[b] + 128 t. A tile running
+  // past its request's rows loads the next request's (or zero-filled OOB)
+  // rows, which are masked like any row past n_b and never stored.
   CUtensorMap qmap;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(g->q_heads),
-                              static_cast<cuuint64_t>(n_new), static_cast<cuuint64_t>(batch)};
+                              static_cast<cuuint64_t>(total), 1};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(D * 2),
                                  static_cast<cuuint64_t>(g->q_heads) * D * 2,
-                                 static_cast<cuuint64_t>(n_new) * g->q_heads * D * 2};
+                                 static_cast<cuuint64_t>(total) * g->q_heads * D * 2};
   const cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(BM), 1};
   int rc = vt::encode_tensor_map_bf16(&qmap, const_cast<void*>(q), 4, dims, strides, box);
   if (rc) return rc;
@@ -551,7 +576,8 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   a.out = static_cast<__nv_bfloat16*>(out);
   a.kv = static_cast<const CUtensorMap*>(kv_maps);
   a.start = start;
-  a.n_new = n_new;
+  a.q_off = q_off;
+  a.n_new = max_n_new;
   a.hq = g->q_heads;
   a.hkv = g->kv_heads;
   a.tpc = g->tokens_per_chunk;
@@ -559,7 +585,7 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   a.slots = group % kSlots == 0 ? kSlots : 1;  // a pair never straddles two kv heads
   a.batch = batch;
   a.pairs = g->q_heads / a.slots;
-  a.n_qtiles = (n_new + BM - 1) / BM;
+  a.n_qtiles = (max_n_new + BM - 1) / BM;
   a.n_items = a.n_qtiles * a.pairs * batch;
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t smem = sizeof(Smem) + 1024;
@@ -574,4 +600,23 @@ extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, cons
   const int grid = a.n_items < n_sm ? a.n_items : n_sm;  // persistent: one CTA per SM
   prefill_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(qmap, a);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" int vt_prefill_attention(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                    const void* kv_maps, const int32_t* start, int32_t batch,
+                                    int32_t n_new, float scale, void* out, void* stream) {
+  return launch_prefill(g, layer, q, kv_maps, start, nullptr, batch, n_new,
+                        static_cast<int64_t>(batch) * n_new, scale, out, stream);
+}
+
+extern "C" int vt_prefill_attention_varlen(const vt_kv_geometry* g, int32_t layer, const void* q,
+                                           const void* kv_maps, const int32_t* start,
+                                           const int32_t* q_offsets, int32_t batch,
+                                           int32_t max_n_new, int64_t total_tokens, float scale,
+                                           void* out, void* stream) {
+  if (!q_offsets) return cudaErrorInvalidValue;
+  return launch_prefill(g, layer, q, kv_maps, start, q_offsets, batch, max_n_new, total_tokens,
+                        scale, out, stream);
 }

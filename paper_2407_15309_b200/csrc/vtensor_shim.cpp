@@ -641,6 +641,22 @@ struct vt_device {
 
 namespace {
 
+// Makes the device's context current on the calling thread for one call and
+// restores whatever was current before (the caller's CUDA runtime state, e.g.
+// torch on another GPU of the same process, must not see a foreign context).
+struct CtxScope {
+  CUcontext prev = nullptr;
+  bool swapped = false;
+  explicit CtxScope(vt_device* d) {
+    Driver& drv = driver();
+    drv.CtxGetCurrent(&prev);
+    if (prev != d->ctx) swapped = drv.CtxSetCurrent(d->ctx) == CUDA_SUCCESS;
+  }
+  ~CtxScope() {
+    if (swapped) driver().CtxSetCurrent(prev);
+  }
+};
+
 int check_map_args(vt_device* d, int64_t base, int64_t page, int64_t id, RangeState** out) {
   auto it = d->ranges.find(base);
   if (it == d->ranges.end())
@@ -742,7 +758,7 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
       delete d;
       return code;
     };
-    d->ensure_ctx();
+    CtxScope scope(d);
     d->prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     d->prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     d->prop.location.id = cuda_ordinal;
@@ -783,7 +799,7 @@ int vt_dev_close(vt_device* d) {
     if (d->worker.joinable()) d->worker.join();
     d->stop_pool();
     Driver& drv = driver();
-    d->ensure_ctx();
+    CtxScope scope(d);
     d->drain_reserve();
     // Tear down whatever the manager left behind (caller is responsible for
     // having synchronised the streams that read these pages).
@@ -824,7 +840,7 @@ int vt_reserve(vt_device* d, int64_t size, int64_t* base, int64_t* pages) {
   rs.pages = n;
   rs.slot.assign(static_cast<size_t>(n), -1);
   if (d->is_cuda()) {
-    d->ensure_ctx();
+    CtxScope scope(d);
     CUdeviceptr va = 0;
     CUresult r = driver().AddrReserve(&va, static_cast<size_t>(size),
                                       static_cast<size_t>(page), 0, 0);
@@ -1131,7 +1147,7 @@ int vt_poll(const vt_device* d, uint64_t ticket, int* done) {
 
 int vt_fence(vt_device* d, void* stream) {
   if (!d->is_cuda()) return VT_OK;
-  d->ensure_ctx();
+  CtxScope scope(d);
   Driver& drv = driver();
   // Route every fence through the one in-order fence stream: epoch e then
   // completes only after all earlier fences, whichever streams they named, so

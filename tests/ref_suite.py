@@ -61,14 +61,24 @@ LINKED = ("__init__.py", "engine.py", "metrics.py", "trace.py", "verify.py", "ba
           "cli.py")
 
 
-def build_kvsim_overlay(root: str) -> str:
+def kvsim_source() -> str | None:
+    """The reference kvsim sources: /root/reference here, else the unmodified
+    install under baseline/_ref (it travels to the GPU box with the repo)."""
+    for d in (REF_SRC, os.path.join(REPO, "baseline", "_ref", "kvsim")):
+        if os.path.isfile(os.path.join(d, "engine.py")):
+            return d
+    return None
+
+
+def build_kvsim_overlay(root: str, src: str | None = None) -> str:
+    src = src or REF_SRC
     pkg = os.path.join(root, "kvsim")
     os.makedirs(pkg, exist_ok=True)
     for name, body in SHIMS.items():
         with open(os.path.join(pkg, name), "w") as f:
             f.write(body)
     for name in LINKED:
-        os.symlink(os.path.join(REF_SRC, name), os.path.join(pkg, name))
+        os.symlink(os.path.join(src, name), os.path.join(pkg, name))
     return root
 
 

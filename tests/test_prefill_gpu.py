@@ -115,3 +115,45 @@ def test_shared_prefix_is_the_same_physical_memory(cuda_ok):
     torch.cuda.synchronize()
     k_b2, _ = read_kv(vas[0], 16, 3, st.geo)
     assert torch.all(k_b2 == 1.5)
+
+
+VARLEN_CASES = {
+    # name: (layers, kv_heads, q_heads, max_seq, [(start, n_new), ...])
+    "engine_step_mix_gqa4": (32, 8, 32, 4096, [(2048, 512), (0, 130), (100, 1), (2048, 37),
+                                               (300, 700), (0, 128), (17, 129)]),
+    "toy_mha_tpc512": (1, 8, 8, 4096, [(0, 256), (0, 3000), (512, 700), (1000, 1)]),
+    "single_request": (16, 2, 16, 2048, [(640, 130)]),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(VARLEN_CASES))
+def test_varlen_prefill_matches_oracle(cuda_ok, name):
+    """One launch prefills requests with different prefix lengths and
+    different numbers of new tokens (the engine's admitted batch,
+    kvsim/engine.py:422-484, 500-504), q/out packed cu_seqlens-style."""
+    from paper_2407_15309_b200.attention import prefill_attention_varlen
+    from vt_gpu_util import admit_with_lengths
+
+    layers, hkv, hq, max_seq, reqs = VARLEN_CASES[name]
+    st = cuda_stack(layers, hkv, hq, max_seq, capacity_chunks=4096)
+    kv_len = [s + n for s, n in reqs]
+    kv_va, _ = admit_with_lengths(st, kv_len, seed=len(name))
+    offs = [0]
+    for _, n in reqs:
+        offs.append(offs[-1] + n)
+    gen = torch.Generator(device="cuda").manual_seed(99)
+    q = torch.randn(offs[-1], hq, 128, generator=gen, device="cuda").to(torch.bfloat16)
+    maps = kv_tensor_maps(kv_va.tolist(), kv_len, st.geo)
+    start = torch.tensor([s for s, _ in reqs], dtype=torch.int32, device="cuda")
+    q_off = torch.tensor(offs, dtype=torch.int32, device="cuda")
+    out = torch.full_like(q, float("nan"))  # every row must be written
+    layer = layers - 1
+    prefill_attention_varlen(q, maps, start, q_off, max(n for _, n in reqs), layer, st.geo, out=out)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    for b, (s, n) in enumerate(reqs):
+        k, v = read_kv(int(kv_va[b]), s + n, layer, st.geo)
+        ref = prefill_attention_ref(q[offs[b]:offs[b + 1]].cpu(), k.cpu(), v.cpu(), s)
+        err = rel_err(out[offs[b]:offs[b + 1]].cpu(), ref)
+        assert err <= TOL, f"{name} request {b} (start {s}, n {n}): rel err {err:.3e}"

@@ -128,3 +128,42 @@ def test_prefix_shared_across_processes(cuda_ok):
     assert identity_ok
     assert ksum == float(k.float().sum()) and vabs == float(v.float().abs().sum())
     assert p.exitcode == 0
+
+
+@pytest.mark.gpu
+def test_prefix_shared_across_gpus(cuda_ok):
+    """the donor's pool on GPU 0, the borrower's on GPU 1.
+    The imported chunks stay in GPU 0's HBM; the borrower's cuMemSetAccess
+    grants GPU 1 access to them (peer over NVLink), and GPU 1's prefill kernel
+    reads the shared prefix in place through the borrower's VA."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (the driver's multi-GPU box)")
+    with torch.cuda.device(0):
+        donor, base, dva = _donor(seed=7)
+        tokens = base + [9000 + k for k in range(NEW)]
+        shared = export_prefix(donor.sched, tokens)
+    with torch.cuda.device(1):
+        borrower = cuda_stack(32, 8, 32, 4096, capacity_chunks=512)
+        assert borrower.dev.cuda_ordinal == 1
+        tpc = borrower.cfg.tokens_per_chunk
+        rm, stats = import_prefix(borrower.sched, "turn", tokens, shared)
+        assert stats.identity_ok and stats.shared_tokens == PREFIX
+        borrower.dev.wait()
+        bva = borrower.dev.va(rm.vt.space.rng)
+        own = chunk_view(bva, (PREFIX + NEW) // tpc, borrower.geo)[PREFIX // tpc:]
+        own.copy_(torch.randn(own.shape, device="cuda:1").to(torch.bfloat16))
+        q = torch.randn(1, NEW, 32, 128, device="cuda:1").to(torch.bfloat16)
+        maps = kv_tensor_maps([bva], [PREFIX + NEW], borrower.geo, device="cuda:1")
+        out = prefill_attention(q, maps, torch.tensor([PREFIX], dtype=torch.int32, device="cuda:1"),
+                                11, borrower.geo)
+        torch.cuda.synchronize()
+        k_b, v_b = read_kv(bva, PREFIX + NEW, 11, borrower.geo)
+    with torch.cuda.device(0):
+        k_d, v_d = read_kv(dva, PREFIX, 11, donor.geo)
+    assert torch.equal(k_d.cpu(), k_b[:, :PREFIX].cpu()) and torch.equal(v_d.cpu(), v_b[:, :PREFIX].cpu())
+    ref = prefill_attention_ref(q[0].cpu(), k_b.cpu(), v_b.cpu(), PREFIX)
+    assert rel_err(out[0].cpu(), ref) <= 2e-2
+    with torch.cuda.device(1):
+        borrower.sched.mark_prefilled("turn")
+        borrower.sched.release("turn")
+        borrower.dev.wait()
