@@ -7,7 +7,7 @@ The attention half (decode split-KV, tcgen05 prefill, KV append) lives in
 ``libvtattn.so`` and is reached through :mod:`paper_2407_15309_b200.attention`.
 """
 
-from .geometry import GIB, KIB, MIB, ModelGeometry, SimConfig, format_size, parse_size
+from .geometry import GIB, KIB, MIB, ModelGeometry, SimConfig
 from .vmm import (
     ChunkStillMapped,
     DeviceCall,
@@ -45,7 +45,7 @@ from .vts import AdmitStats, ExceedsMaxSeqLen, RequestMem, VTensorScheduler
 __version__ = "0.1.0"
 
 __all__ = [
-    "GIB", "KIB", "MIB", "ModelGeometry", "SimConfig", "format_size", "parse_size",
+    "GIB", "KIB", "MIB", "ModelGeometry", "SimConfig",
     "ChunkStillMapped", "DeviceCall", "DeviceConfig", "DeviceError", "DeviceOutOfMemory",
     "DeviceStats", "DriverFailure", "IndexOutOfRange", "InvalidSize", "PageAlreadyMapped",
     "PageNotMapped", "PhysicalHandle", "RangeStillMapped", "StaleHandle", "UnknownRange",

@@ -26,8 +26,15 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SHIMS = {
     "config.py": (
-        "from paper_2407_15309_b200.geometry import (GIB, KIB, MIB, ModelGeometry, "
-        "SimConfig, format_size, parse_size)\n"
+        "from paper_2407_15309_b200.geometry import GIB, KIB, MIB, ModelGeometry, SimConfig\n"
+        # CLI size parsing is out of scope: the reference's own
+        "import importlib.util as _u\n"
+        "_s = _u.spec_from_file_location('_kvsim_ref_config', {ref_config!r})\n"
+        "_m = _u.module_from_spec(_s)\n"
+        "import sys as _sys\n"
+        "_sys.modules['_kvsim_ref_config'] = _m\n"
+        "_s.loader.exec_module(_m)\n"
+        "parse_size, format_size = _m.parse_size, _m.format_size\n"
     ),
     "device.py": (
         "from paper_2407_15309_b200.vmm import (ChunkStillMapped, DeviceCall, DeviceConfig, "
@@ -76,7 +83,7 @@ def build_kvsim_overlay(root: str, src: str | None = None) -> str:
     os.makedirs(pkg, exist_ok=True)
     for name, body in SHIMS.items():
         with open(os.path.join(pkg, name), "w") as f:
-            f.write(body)
+            f.write(body.replace("{ref_config!r}", repr(os.path.join(src, "config.py"))))
     for name in LINKED:
         os.symlink(os.path.join(src, name), os.path.join(pkg, name))
     return root
