@@ -21,11 +21,14 @@
 //   share of the weight is ONE contiguous byte range pulled with 16 KiB bulk
 //   copies (no tensor map, sequential DRAM pages).
 // * K split over a CTA pair (thread-block cluster of 2). Each feature tile is
-//   computed by two CTAs, one per half of `hidden`; once the lower CTA's MMAs
-//   are done (its ring is idle) the upper CTA writes its fp32 partial straight
-//   from TMEM into that ring with asynchronous remote stores (st.async over
-//   distributed shared memory, each completing its bytes on the lower CTA's
-//   mbarrier); the lower CTA adds it and stores. The reduction never touches
+//   computed by two CTAs, one per half of `hidden`, and each CTA finalises half
+//   of the token columns: once both CTAs' MMAs are done (their rings are idle)
+//   each writes the fp32 partial of the OTHER half straight from TMEM into the
+//   peer's ring with asynchronous remote stores (st.async over distributed
+//   shared memory, completing bytes on the peer's mbarrier), then adds the
+//   peer's partial of its own half and stores it — the hand-off and the
+//   stores split evenly over the pair (one-directional, with the lower CTA
+//   storing everything, the tail was 2.5 us). The reduction never touches
 //   global memory. Measured alternatives (tools/trace_qkv.py
 //   timelines): a global split-K reduction (fp32 partials in L2 + arrival
 //   counter) with a stream-K split over every SM streamed the weight at
@@ -68,7 +71,7 @@ struct Cfg {
   static constexpr int kStages = kRingBytes / kStageBytes;
   static constexpr int kTmemCols = NT;
   static_assert(kStages >= 2, "ring too small");
-  static_assert(NT * BM * 4 <= kRingBytes, "the peer partial must fit the ring");
+  static_assert(NT / 2 * BM * 4 <= kRingBytes, "the peer's half partial must fit the ring");
 };
 
 struct Args {
@@ -126,8 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   __shared__ uint64_t full[C::kStages], empty[C::kStages], acc_full;
-  __shared__ uint64_t peer_ready;    // (upper CTA) the lower CTA's ring is free
-  __shared__ uint64_t partial_full;  // (lower CTA) the upper CTA's partial has landed
+  __shared__ uint64_t peer_ready;    // the peer CTA's ring is free (its MMAs are done)
+  __shared__ uint64_t partial_full;  // the peer's partial of our token half has landed
   __shared__ uint64_t row_dst[NT];   // destination of each token's 256-byte head row
   __shared__ __align__(16) __nv_bfloat16 stage_out[4][16][32];  // per epilogue warp
   __shared__ uint32_t tmem_base;
@@ -231,11 +234,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // this thread's output feature within the tile
     const int ep = threadIdx.x - 64;      // 0..127
-    float* peer_part = reinterpret_cast<float*>(ring);  // [NT][BM] fp32 partial (lower CTA)
-    if (half == 0) {
+    // With a CTA pair each CTA finalises half of the token columns: it sends
+    // its partial of the OTHER half to the peer and adds the peer's partial of
+    // its own half, so hand-off and stores are split evenly across the pair.
+    constexpr int kHalfNT = KS == 2 ? NT / 2 : NT;
+    const int my_c0 = static_cast<int>(half) * kHalfNT;          // token columns finalised here
+    const int peer_c0 = KS == 2 ? (1 - static_cast<int>(half)) * kHalfNT : 0;
+    float* peer_part = reinterpret_cast<float*>(ring);  // [kHalfNT][BM] fp32 partial from the peer
+    {
       const int kind = m < a.hq ? 0 : (m < a.hq + a.hkv ? 1 : 2);  // q | K | V
       const int head = kind == 0 ? m : (kind == 1 ? m - a.hq : m - a.hq - a.hkv);
-      for (int i = ep; i < NT; i += 128) {
+      for (int i = my_c0 + ep; i < my_c0 + kHalfNT; i += 128) {
         const int t = tt * NT + i;
         uint64_t dst = 0;
         if (t < a.n_tokens) {
@@ -259,19 +268,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::fence_after();
     if (ep == 0) QKV_TRACE(6);
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    if (KS == 2 && half == 1) {
-      // upper half: once the lower CTA's MMAs are done (its ring is free),
-      // asynchronous remote stores of the fp32 partial straight from the
-      // accumulator, each completing its bytes on the lower CTA's barrier
+    if constexpr (KS == 2) {
+      // our MMAs are done, so our ring is free for the peer's partial; once
+      // the peer's is free too, asynchronous remote stores of the peer's half
+      // straight from the accumulator, completing bytes on its barrier
+      if (ep == 0) {
+        mbar_arrive_expect_tx(&partial_full, kHalfNT * BM * 4);
+        arrive_peer(peer_addr(&peer_ready, 1 - half));
+      }
       mbar_wait(&peer_ready, 0);
       if (ep == 0) QKV_TRACE(7);
-      const uint32_t dst = peer_addr(peer_part, 0);
-      const uint32_t bar = peer_addr(&partial_full, 0);
+      const uint32_t dst = peer_addr(peer_part, 1 - half);
+      const uint32_t bar = peer_addr(&partial_full, 1 - half);
 #pragma unroll 1
-      for (int c = 0; c < NT; c += 32) {
+      for (int c = 0; c < kHalfNT; c += 32) {
         uint32_t r0[16], r1[16];
-        tc::ld16(lane_addr + c, r0);
-        tc::ld16(lane_addr + c + 16, r1);
+        tc::ld16(lane_addr + peer_c0 + c, r0);
+        tc::ld16(lane_addr + peer_c0 + c + 16, r1);
         tc::wait_ld();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -285,49 +298,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                        : "memory");
         }
       }
+      mbar_wait(&partial_full, 0);
       if (ep == 0) QKV_TRACE(8);
-    } else {
-      if (KS == 2) {
-        if (ep == 0) {
-          mbar_arrive_expect_tx(&partial_full, NT * BM * 4);
-          arrive_peer(peer_addr(&peer_ready, 1));  // our ring is free
-        }
-        mbar_wait(&partial_full, 0);
-        if (ep == 0) QKV_TRACE(8);
-      }
+    }
 #pragma unroll 1
-      for (int c = 0; c < NT; c += 32) {
-        uint32_t r0[16], r1[16];
-        tc::ld16(lane_addr + c, r0);
-        tc::ld16(lane_addr + c + 16, r1);
-        tc::wait_ld();
-        float v[32];
+    for (int c = 0; c < kHalfNT; c += 32) {
+      uint32_t r0[16], r1[16];
+      tc::ld16(lane_addr + my_c0 + c, r0);
+      tc::ld16(lane_addr + my_c0 + c + 16, r1);
+      tc::wait_ld();
+      float v[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[i] = __uint_as_float(r0[i]);
-          v[16 + i] = __uint_as_float(r1[i]);
+      for (int i = 0; i < 16; ++i) {
+        v[i] = __uint_as_float(r0[i]);
+        v[16 + i] = __uint_as_float(r1[i]);
+      }
+      if (KS == 2) {  // two K halves: one fp32 add (commutative, so bit-reproducible)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += peer_part[(c + i) * BM + row];
+      }
+      // transpose through this warp's staging tile (16 tokens x 32
+      // features), then 16-byte stores (4 per 64-byte token row segment)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          stage_out[quarter][i][lane] = __float2bfloat16_rn(v[h * 16 + i]);
+        __syncwarp();
+#pragma unroll
+        for (int j = lane; j < 64; j += 32) {
+          const uint64_t dst = row_dst[my_c0 + c + h * 16 + (j >> 2)];
+          if (dst)
+            *reinterpret_cast<uint4*>(dst + quarter * 64 + (j & 3) * 16) =
+                *reinterpret_cast<const uint4*>(&stage_out[quarter][j >> 2][(j & 3) * 8]);
         }
-        if (KS == 2) {  // lower half + upper half: a fixed order, bit-reproducible
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += peer_part[(c + i) * BM + row];
-        }
-        // transpose through this warp's staging tile (16 tokens x 32
-        // features), then 16-byte stores (4 per 64-byte token row segment)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            stage_out[quarter][i][lane] = __float2bfloat16_rn(v[h * 16 + i]);
-          __syncwarp();
-#pragma unroll
-          for (int j = lane; j < 64; j += 32) {
-            const uint64_t dst = row_dst[c + h * 16 + (j >> 2)];
-            if (dst)
-              *reinterpret_cast<uint4*>(dst + quarter * 64 + (j & 3) * 16) =
-                  *reinterpret_cast<const uint4*>(&stage_out[quarter][j >> 2][(j & 3) * 8]);
-          }
-          __syncwarp();
-        }
+        __syncwarp();
       }
     }
     if (ep == 0) QKV_TRACE(9);

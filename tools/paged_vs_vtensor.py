@@ -1,7 +1,12 @@
 """Restate the paper's kernel comparison on B200:
-vTensor decode (no block table) vs a paged-KV decode (block table, same data)
-on config 2. 32 back-to-back layer launches each; same bytes, same kernel
-family. Prints one JSON line."""
+vTensor decode (no block table) vs paged-KV decode (block table, same data)
+on config 2 (B 64, ctx 4096, 32 q / 8 kv heads). Arms: this package's
+tcgen05 and CUDA-core vTensor kernels, the same CUDA-core kernel through a
+block table, and the paged kernels shipped in the image — flashinfer's sm100
+trtllm-gen decode and vLLM's PagedAttention v2 (tests/paged_libs.py), page
+size 16 = one 2 MiB chunk. 32 back-to-back launches each (1 GiB of KV per
+launch, far above L2); every arm's output is checked against the CPU oracle
+on sampled requests. Prints one JSON line."""
 
 import json
 import os
@@ -15,8 +20,10 @@ import torch  # noqa: E402
 
 from paper_2407_15309_b200.attention import (DecodeWorkspace, decode_attention,  # noqa: E402
                                              decode_attention_paged, kv_tensor_maps)
+from oracle.attention_ref import decode_attention_ref, rel_err  # noqa: E402
+from paged_libs import BUILDERS, gather_pages  # noqa: E402
 from test_decode_gpu import build_paged_copy  # noqa: E402
-from vt_gpu_util import admit_with_lengths, cuda_stack  # noqa: E402
+from vt_gpu_util import admit_with_lengths, cuda_stack, gather  # noqa: E402
 
 
 def timed32(fn, L=32, reps=3):
@@ -60,13 +67,37 @@ def main():
     res["vtensor_tcgen05_auto"] = timed32(
         lambda l: decode_attention(q, kv_va, seq, l, st.geo, ctx, out=out, workspace=ws,
                                    kv_maps=maps))
+    # the libraries' paged kernels over one layer's bytes (layer 0) in their own layouts
+    check, unavailable = {}, {}
+    picks = [0, 21, 42, 63]
+    ks, vs = gather(st, kv_va, [ctx] * B, 0)
+    ref = decode_attention_ref(q[picks].cpu(), [ks[i] for i in picks], [vs[i] for i in picks])
+    out0 = decode_attention(q, kv_va, seq, 0, st.geo, ctx, workspace=ws, kv_maps=maps)
+    torch.cuda.synchronize()
+    check["vtensor_tcgen05_auto"] = rel_err(out0[picks].cpu(), ref)
+    del ks, vs
+    K, V, table = gather_pages(st, kv_va, [ctx] * B, 0)
+    for name, build in BUILDERS.items():
+        try:
+            run = build(K, V, table, [ctx] * B, 32)
+            o = run(q, torch.empty_like(q))
+            torch.cuda.synchronize()
+            check[name] = rel_err(o[picks].cpu(), ref)
+            res[name] = timed32(lambda l: run(q, out))
+        except Exception as exc:  # a baseline that cannot run here is reported, not fatal
+            unavailable[name] = str(exc).splitlines()[0][:300] if str(exc) else repr(exc)
     gbs = {k: round(nbytes / (v * 1e-6) / 1e9, 1) for k, v in res.items()}
     best_paged = min(v for k, v in res.items() if k.startswith("paged"))
+    libs = {k: v for k, v in res.items() if k in BUILDERS}
     print(json.dumps({"config": "cfg2 B64 ctx4096 32q/8kv, 32 back-to-back layers",
                       "us_per_layer": {k: round(v, 2) for k, v in res.items()}, "GB/s": gbs,
                       "speedup_vtensor_tc_over_best_paged": round(best_paged / res["vtensor_tcgen05_auto"], 3),
                       "speedup_vtensor_cc_over_paged_same_kernel": round(
-                          res["paged_cuda_core_split1024"] / res["vtensor_cuda_core_split1024"], 3)}))
+                          res["paged_cuda_core_split1024"] / res["vtensor_cuda_core_split1024"], 3),
+                      "speedup_vtensor_tc_over_library": {
+                          k: round(v / res["vtensor_tcgen05_auto"], 3) for k, v in libs.items()},
+                      "oracle_rel_err": {k: round(v, 5) for k, v in check.items()},
+                      "unavailable": unavailable}))
 
 
 if __name__ == "__main__":
