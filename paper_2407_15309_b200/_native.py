@@ -96,6 +96,10 @@ class VtDriverStats(ctypes.Structure):
 
 def _load(name: str) -> ctypes.CDLL:
     path = os.path.join(_HERE, name)
+    # A/B experiments only (tools/): load a variant build of the same library
+    override = os.environ.get("VT_LIB_" + name.split(".")[0].upper())
+    if override:
+        path = override
     if not os.path.exists(path):
         raise ImportError(
             f"{name} is not built ({path} missing); run __graft_entry__.build() "

@@ -461,7 +461,7 @@ static int decode_impl(const vt_kv_geometry* g, int32_t layer, const void* q,
   g_last_launches = 0;
   if (g->head_dim != kD || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
   const int G = g->q_heads / g->kv_heads;
-  const bool tc = kv_maps != nullptr && batch <= 1024;
+  const bool tc = kv_maps != nullptr;  // any batch (no silent switch of kernel family)
   const int split = split_tokens > 0 ? split_tokens
                     : tc             ? tc_split(batch, g->kv_heads, max_seq_len, num_sms())
                                      : default_split(max_seq_len, false);

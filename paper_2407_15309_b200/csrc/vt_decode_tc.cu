@@ -50,6 +50,8 @@ constexpr uint32_t kTmemCols = 64;
 constexpr uint32_t kSCol = 0;   // S^T buffers at columns 0 and 16
 constexpr uint32_t kOCol = 32;  // per-tile O^T buffers at columns 32 and 48
 
+constexpr int kLensSmem = 1024;
+
 struct __align__(1024) Smem {
   __nv_bfloat16 k[KSTAGES][2][TILE * 64];  // SW128 K-major (tok x d)
   __nv_bfloat16 v[VSTAGES][2][TILE * 64];  // SW128, read as MN-major A (d x tok)
@@ -61,7 +63,7 @@ struct __align__(1024) Smem {
     float lpart[4][MAXG];
     float m[MAXG];
   } epi[2];
-  int32_t lens[1024];                      // seq_lens staged once (batch <= 1024)
+  int32_t lens[kLensSmem];                 // seq_lens of the first kLensSmem requests, staged once
   uint64_t k_full[KSTAGES], k_empty[KSTAGES];
   uint64_t v_full[VSTAGES], v_empty[VSTAGES];
   uint64_t q_full[2], q_empty[2];
@@ -95,7 +97,7 @@ __device__ __forceinline__ bool unit_of(const Args& a, const int32_t* lens, int 
   const int bh = u % nbh;
   w.h = bh % a.hkv;
   w.b = bh / a.hkv;
-  const int len = lens[w.b];
+  const int len = w.b < kLensSmem ? lens[w.b] : __ldg(a.seq_lens + w.b);  // larger batches: L1/L2
   w.t0 = w.s * a.split_tok;
   w.t1 = min(len, w.t0 + a.split_tok);
   w.splits_b = (len + a.split_tok - 1) / a.split_tok;
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == 1) tc::alloc(&sm.tmem_base, kTmemCols);
-  for (int i = threadIdx.x; i < a.batch; i += kThreads) sm.lens[i] = a.seq_lens[i];
+  for (int i = threadIdx.x; i < min(a.batch, kLensSmem); i += kThreads) sm.lens[i] = a.seq_lens[i];
   // P^T rows G..15 are never written: zero the whole buffer once.
   for (int i = threadIdx.x; i < 4 * NQ * 64 / 8; i += kThreads)
     reinterpret_cast<uint4*>(&sm.p[0][0][0])[i] = make_uint4(0, 0, 0, 0);

@@ -79,7 +79,7 @@ struct __align__(1024) Smem {
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[kSlots];
-  uint64_t p_full[kSlots];
+  uint64_t p_full[kSlots][2];  // P of keys 0-63 / 64-127 of the block is in TMEM
   uint64_t o_done[kSlots];
   uint32_t tmem_base;
 };
@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&sm.s_full[s], 1);
-      mbar_init(&sm.p_full[s], 128);
+      mbar_init(&sm.p_full[s][0], 128);
+      mbar_init(&sm.p_full[s][1], 128);
       mbar_init(&sm.o_done[s], 1);
     }
     fence_mbar_init();
@@ -320,15 +321,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::commit(&sm.s_full[s]);
       };
-      auto mma_pv = [&](int s, int g, bool first) {  // elected lane only
+      // O += P V over keys [64 hf, 64 hf + 64) of the block (4 MMAs of K16):
+      // the softmax hands P over in two halves so the first half's MMAs run
+      // while it still exponentiates the second.
+      auto mma_pv_half = [&](int s, int g, int hf, bool first) {  // elected lane only
         const uint32_t b0 = lv + static_cast<uint32_t>((g % kStages) * 2048);
         const uint32_t d = tmem + kOCol + static_cast<uint32_t>(s * D);
         const uint32_t p = tmem + static_cast<uint32_t>(s * BN);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
+        for (int k4 = 0; k4 < BN / 32; ++k4) {
+          const int kk = hf * (BN / 32) + k4;
           tc::mma_ts(d, p + 8 * kk, b0 + static_cast<uint32_t>(kk * 128), hi, id_pv,
                      (!first || kk > 0) ? 1u : 0u);
-        tc::commit(&sm.o_done[s]);
+        }
+        if (hf == 1) tc::commit(&sm.o_done[s]);
       };
       int g = 0, n = 0;
       for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
@@ -355,10 +361,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int s = 0; s < kSlots; ++s) {
             if (s < nslots) {
               const bool last_slot = s == nslots - 1;
-              wait_fence(&sm.p_full[s], g & 1);
+              wait_fence(&sm.p_full[s][0], g & 1);
+              if (tc::elect_one()) mma_pv_half(s, g, 0, j == 0);
+              __syncwarp();
+              wait_fence(&sm.p_full[s][1], g & 1);
               VT_TRACE(lane == 0, g, 4 + s);
               if (tc::elect_one()) {
-                mma_pv(s, g, j == 0);
+                mma_pv_half(s, g, 1, j == 0);
                 if (last_slot) tc::commit(&sm.v_empty[g % kStages]);
                 if (more) {
                   mma_s(s, g + 1);
@@ -434,30 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float m_use = m_new == -INFINITY ? 0.f : m_new;
           const float2 sl2v = make_float2(sl2, sl2);
           const float2 negm = make_float2(-m_use, -m_use);
-          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                           make_float2(0.f, 0.f)};
-          uint32_t pr[BN / 2];
-#pragma unroll
-          for (int k = 0; k < BN / 2; ++k) {
-            float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
-            if ((kPolyMask >> (k & 7)) & 1u) {
-              e = ex2_poly2(e);
-            } else {
-              e.x = tc::ex2(e.x);
-              e.y = tc::ex2(e.y);
-            }
-            acc[k & 3] = __fadd2_rn(acc[k & 3], e);
-            pr[k] = pack_bf16(e.x, e.y);
-          }
-          const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
-          l_run = fmaf(l_run, alpha, a01.x + a01.y);
-          m_run = m_new;
-          VT_SUB(row == 0 && s == 0 && l_run > -1.f, g, 2);
-          // P -> TMEM over the first 64 S columns: column c = keys (2c, 2c+1) as bf16x2.
-          tmem_st32(s_addr, pr);
-          tmem_st32(s_addr + 32, pr + 32);
           if (j >= 1 && __any_sync(0xffffffffu, grow)) {
-            // PV(j-1) is complete: S(j) was issued after it and has completed.
+            // Lazy rescale of O before any of this block's PV: PV(j-1) is
+            // complete (S(j), issued after it, has completed).
             mbar_wait(&sm.o_done[s], (g - 1) & 1);
             tc::fence_after();
 #pragma unroll
@@ -489,11 +477,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             zeroed = true;
           }
-          tc::wait_st();
+          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+          // Two halves of 64 keys: P of keys 0-63 goes to TMEM columns 0-31 and
+          // is handed to the MMA warp (its PV half runs) while the second half
+          // is exponentiated. Column c = keys (2c, 2c+1) as bf16x2.
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t pr[BN / 4];
+#pragma unroll
+            for (int k2 = 0; k2 < BN / 4; ++k2) {
+              const int k = hf * (BN / 4) + k2;
+              float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
+              if ((kPolyMask >> (k & 7)) & 1u) {
+                e = ex2_poly2(e);
+              } else {
+                e.x = tc::ex2(e.x);
+                e.y = tc::ex2(e.y);
+              }
+              acc[k & 3] = __fadd2_rn(acc[k & 3], e);
+              pr[k2] = pack_bf16(e.x, e.y);
+            }
+            tmem_st32(s_addr + 32 * hf, pr);
+            tc::wait_st();
+            if (hf == 0 && zeroed) fence_proxy_async_smem();
+            tc::fence_before();
+            mbar_arrive(&sm.p_full[s][hf]);
+          }
+          const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+          l_run = fmaf(l_run, alpha, a01.x + a01.y);
+          m_run = m_new;
           VT_SUB(row == 0 && s == 0, g, 3);
-          if (zeroed) fence_proxy_async_smem();
-          tc::fence_before();
-          mbar_arrive(&sm.p_full[s]);
           VT_TRACE(row == 0, g, 2 * s + 1);
         }
         // epilogue: PV(n_kv-2) completed before S(n_kv-1); wait for the last PV.

@@ -182,3 +182,24 @@ def test_chained_layers_match_oracle(cuda_ok):
         ks, vs = gather(st, kv_va, new_lens, layer)
         ref = decode_attention_ref(q[layer].cpu(), ks, vs)
         assert rel_err(out[layer].cpu(), ref) <= TOL, layer
+
+
+@pytest.mark.gpu
+def test_tcgen05_decode_above_1024_requests(cuda_ok):
+    """Batches beyond the 1024 lengths staged in shared memory stay on the
+    tcgen05 kernel (no silent switch of kernel family) and stay correct."""
+    import random
+
+    rng = random.Random(5)
+    lens = [rng.randint(1, 40) for _ in range(1100)]
+    lens[1099] = 0
+    st = cuda_stack(1, 8, 32, 4096, capacity_chunks=2048)  # tpc 512: one chunk each
+    kv_va, seq = admit_with_lengths(st, lens, seed=8)
+    q = torch.randn(len(lens), 32, 128, device="cuda").to(torch.bfloat16)
+    out = decode_attention(q, kv_va, seq, 0, st.geo, max(lens), kv_maps=mapped_maps(st, kv_va, len(lens)))
+    torch.cuda.synchronize()
+    ks, vs = gather(st, kv_va, lens, 0)
+    pick = [0, 1, 500, 1023, 1024, 1025, 1098, 1099]
+    ref = decode_attention_ref(q[pick].cpu(), [ks[i] for i in pick], [vs[i] for i in pick])
+    assert rel_err(out[pick].cpu(), ref) <= TOL
+    assert torch.all(out[1099] == 0)
