@@ -63,23 +63,40 @@ class Checker:
         self.fail: list[str] = []
 
     def _kv(self, rid, layer, tokens):
+        """Mirror K/V ``[n, H, d]`` of ``tokens`` (positions 0..n-1), grown in
+        place: K/V of a position depends only on (token, position), so the
+        prefix of a longer or restarted request is reused as long as its
+        tokens agree."""
         import torch
 
-        tokens = list(tokens)
-        got = self.mirror.get((rid, layer))
-        if got is not None and got[0] == tokens[:len(got[0])]:
-            n0 = len(got[0])
-            K, V = got[1], got[2]
-        else:
-            n0, K, V = 0, None, None
-        if n0 < len(tokens):
-            t = torch.tensor(tokens[n0:], dtype=torch.int64)
-            p = torch.arange(n0, len(tokens), dtype=torch.int64)
-            k, v = self.ad.source.kv(t, p, layer=layer)  # [n, H, d]
-            K = k if K is None else torch.cat([K, k])
-            V = v if V is None else torch.cat([V, v])
-        self.mirror[(rid, layer)] = (tokens, K, V)
-        return K, V
+        n = len(tokens)
+        ent = self.mirror.get((rid, layer))
+        if ent is None or ent[1].shape[0] < n:
+            cap = max(n, 1024) if ent is None else max(n, 2 * ent[1].shape[0])
+            H, d = self.ad.geo.kv_heads, self.ad.geo.head_dim
+            K = torch.empty(cap, H, d, dtype=torch.bfloat16)
+            V = torch.empty_like(K)
+            have, toks = 0, []
+            if ent is not None:
+                have, toks = ent[0], ent[3]
+                K[:have], V[:have] = ent[1][:have], ent[2][:have]
+            ent = [have, K, V, toks]
+            self.mirror[(rid, layer)] = ent
+        have, K, V, toks = ent
+        # keep the longest prefix whose tokens agree (a preempted request restarts)
+        have = min(have, n)
+        if have and toks[have - 1] != tokens[have - 1]:
+            have = 0
+            while have < n and have < len(toks) and toks[have] == tokens[have]:
+                have += 1
+        if have < n:
+            t = torch.tensor(tokens[have:n], dtype=torch.int64)
+            p = torch.arange(have, n, dtype=torch.int64)
+            k, v = self.ad.source.kv(t, p, layer=layer)  # [n - have, H, d]
+            K[have:n], V[have:n] = k, v
+        ent[0] = n
+        ent[3] = list(tokens) if len(tokens) != len(toks) or have < n else toks
+        return K[:n], V[:n]
 
     def __call__(self, rec):
         import torch
