@@ -218,6 +218,44 @@ def sum_over_ranks(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------- the workload --
+def staggered_lens(ctx: int, B: int, win: int) -> list[int]:
+    """Context lengths staggered over one map-ahead window (`win` tokens):
+    every step some request runs out of headroom and extends."""
+    return [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx for b in range(B)]
+
+
+def workload_config(cfg_name: str, world: int, split: int = 0, path: str = "tcgen05",
+                    growth: bool = False) -> dict:
+    """The bench line's `config` (identical for both arms): the workload one
+    GPU runs per step. Computed without a GPU so the reference arm reports
+    exactly the same dict."""
+    from paper_2407_15309_b200.sharding import head_shard, layer_groups
+
+    L, hkv, hq, B, ctx = CONFIGS[cfg_name]
+    head_partition = cfg_name in HEAD_PARTITIONED
+    if head_partition:
+        sh = head_shard(hkv, hq, world, 0)
+        hkv, hq = sh.local_kv_heads, sh.local_q_heads
+    groups = layer_groups(L, hkv)
+    tpc = 2 * MIB // groups[0][1].bytes_per_token
+    win = int(os.environ.get("VT_MAP_AHEAD", "4")) * tpc
+    lens = [GROWTH_START] * B if growth else staggered_lens(ctx, B, win)
+    span = (f"{GROWTH_START}..{GROWTH_END} (growth trace)" if growth
+            else f"{min(lens)}..{max(lens)}")
+    kv_gib = (GROWTH_END if growth else sum(lens) / B) * B * L * 2 * hkv * 128 * 2 / GIB
+    return {
+        "workload": f"{cfg_name}: decode step, {L} layers, {hq} q / {hkv} kv heads per GPU, "
+                    f"d 128, batch {B}, ctx {span}",
+        "batch_per_gpu": B, "context": ctx, "layers": L,
+        "parallelism": (f"kv-head partition x{world} (no collective)" if head_partition
+                        else f"request partition x{world} (no collective)"),
+        "layer_groups": len(groups),
+        "l2": "inputs larger than L2 (KV working set %.1f GiB)" % kv_gib,
+        "split_tokens": split or "auto",
+        "decode_path": path,
+    }
+
+
 class _Group:
     """One layer group: its own manager (pool/VTO/VTS) on the GPU's shared VMM
     device, geometry (layers_in_group, local kv heads), KV-map cache."""
@@ -303,8 +341,7 @@ class DecodeWorkload:
         else:
             # staggered lengths over one map-ahead window: every step some
             # request runs out of headroom and extends by a `map_ahead` run
-            self.lens = [ctx - (win - 1) + (b * win // B) if ctx >= win else ctx
-                         for b in range(B)]
+            self.lens = staggered_lens(ctx, B, win)
         self.groups = [_Group(self, first, geom, seed + 17 * i)
                        for i, (first, geom) in enumerate(groups)]
         gen = torch.Generator(device="cuda").manual_seed(seed)
@@ -707,18 +744,7 @@ def run_ours(args, world, rank, local):
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (seeded randn bf16 KV in real cuMemMap'd 2 MiB chunks)",
-            "config": {
-                "workload": f"{args.config}: decode step, {wl.L} layers, {wl.hq} q / {wl.hkv} kv "
-                            f"heads per GPU, d 128, batch {wl.B}, ctx {min(wl.lens)}..{max(wl.lens)}",
-                "batch_per_gpu": wl.B, "context": wl.ctx, "layers": wl.L,
-                "parallelism": (f"kv-head partition x{world} (no collective)" if wl.head_partition
-                                else f"request partition x{world} (no collective)"),
-                "layer_groups": len(wl.groups),
-                "l2": "inputs larger than L2 (KV working set %.1f GiB)" % (
-                    sum(wl.host_lens) * wl.kv_bytes_per_token / GIB),
-                "split_tokens": args.split or "auto",
-                "decode_path": args.path,
-            },
+            "config": workload_config(args.config, world, args.split, args.path, args.growth),
             "tokens_per_s": round(tokens_all / (elapsed_max * 1e-3), 1),
             "hbm_frac_of_step": round(value / hbm_peak, 4),
             "roofline": {
@@ -1135,6 +1161,8 @@ def run_reference(args, world, rank):
     import torch
 
     torch.set_num_threads(os.cpu_count() or 1)
+    if args.growth:
+        args.config = "llama3-8b-32k"
     L, hkv, hq, B, ctx = CONFIGS[args.config]
     from oracle.attention_ref import decode_attention_torch_cpu
 
@@ -1161,7 +1189,8 @@ def run_reference(args, world, rank):
         "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+        "data": "synthetic", "config": workload_config(args.config, world, args.split, args.path,
+                                                       args.growth),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s",
                          "cores": torch.get_num_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,

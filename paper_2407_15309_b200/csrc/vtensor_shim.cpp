@@ -236,6 +236,7 @@ struct vt_device {
   size_t job_n = 0;
   uint64_t job_gen = 0;
   bool pool_stop = false;
+  int job_active = 0;  // pool threads inside the current job (guarded by pool_mu)
   std::atomic<size_t> job_next{0}, job_left{0};
   int driver_threads = 1;
   std::mutex lat_mu;
@@ -398,6 +399,10 @@ struct vt_device {
   // completes 0.5-1.6 map+SetAccess per ms (each call waits 150-720 us on the
   // driver, not the CPU), four threads 2-6 per ms, and none of it slows the
   // HBM-streaming kernels running meanwhile.
+  // A job is closed only when every item ran AND every pool thread that
+  // joined it has left it (job_fn is cleared first, so no thread can join
+  // late): a thread still inside run_job_items must never claim an item of
+  // the next job with this job's (by then destroyed) function.
   void parallel_for(size_t n, const std::function<void(size_t)>& fn) {
     if (n == 0) return;
     if (n == 1 || pool.empty()) {
@@ -417,6 +422,7 @@ struct vt_device {
     std::unique_lock<std::mutex> lk(pool_mu);
     pool_done_cv.wait(lk, [&] { return job_left.load() == 0; });
     job_fn = nullptr;
+    pool_done_cv.wait(lk, [&] { return job_active == 0; });
   }
   void run_job_items(const std::function<void(size_t)>& fn, size_t n) {
     for (;;) {
@@ -442,8 +448,14 @@ struct vt_device {
         seen = job_gen;
         fn = job_fn;
         n = job_n;
+        ++job_active;
       }
       run_job_items(*fn, n);
+      {
+        std::lock_guard<std::mutex> lk(pool_mu);
+        --job_active;
+      }
+      pool_done_cv.notify_all();
     }
   }
   void start_pool(int threads) {
