@@ -99,6 +99,7 @@ class Checker:
         return K[:n], V[:n]
 
     def __call__(self, rec):
+        import numpy as np
         import torch
 
         from oracle.attention_ref import decode_attention_ref, prefill_attention_ref, rel_err
@@ -123,8 +124,18 @@ class Checker:
                         torch.full((n - s,), HashedTokenSource.request_key(r), dtype=torch.int64),
                         torch.arange(s, n), layer=layer)
                     assert torch.equal(q, pf["q"][layer, a:b].cpu())
-                    ref = prefill_attention_ref(q, K.permute(1, 0, 2), V.permute(1, 0, 2), s)
-                    self._note(rel_err(out[a:b], ref), f"step {step} prefill {r} layer {layer}")
+                    if n - s <= 256:  # whole causal block
+                        ref = prefill_attention_ref(q, K.permute(1, 0, 2), V.permute(1, 0, 2), s)
+                        got = out[a:b]
+                    else:  # sampled query rows: row i is a decode over keys [0, s + i]
+                        rows = sorted({0, 1, 127, 128, (n - s) // 2, n - s - 2, n - s - 1}
+                                      | {(i * 7919) % (n - s) for i in range(9)})
+                        ref = np.concatenate([
+                            decode_attention_ref(q[i:i + 1], [K[:s + i + 1].permute(1, 0, 2)],
+                                                 [V[:s + i + 1].permute(1, 0, 2)])
+                            for i in rows])
+                        got = out[a:b][rows]
+                    self._note(rel_err(got, ref), f"step {step} prefill {r} layer {layer}")
                     self.checked_prefill += 1
             if "decode" in rec and self.every and step % self.every == 0:
                 dc = rec["decode"]
