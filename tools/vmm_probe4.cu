@@ -161,15 +161,29 @@ int main(int argc, char** argv) {
       for (int i = 0; i < 16; ++i) CK(cuMemUnmap(probe_va + CH * i, CH));
     }
     for (auto h : hs) CK(cuMemRelease(h));
+    // slab creates: one allocation of `slab` chunks, cost per 2 MiB chunk
+    double slab_us = 0;
+    if (slab > 1) {
+      std::vector<double> v;
+      for (int i = 0; i < 8; ++i) {
+        CUmemGenericAllocationHandle h;
+        double t0 = now_us();
+        CK(cuMemCreate(&h, CH * slab, &ap, 0));
+        v.push_back((now_us() - t0) / slab);
+        CK(cuMemRelease(h));
+      }
+      slab_us = med(v);
+    }
     if (load) {
       stop = true;
       launcher.join();
     }
     std::printf(
         "{\"slab\":%d,\"live_chunks\":%d,\"live_allocations\":%zu,\"load\":\"%s\",\"create_us\":%.1f,"
-        "\"map_us\":%.1f,\"setaccess_us\":%.1f,\"unmap_us\":%.1f,\"setaccess_run16_us\":%.1f}\n",
+        "\"map_us\":%.1f,\"setaccess_us\":%.1f,\"unmap_us\":%.1f,\"setaccess_run16_us\":%.1f,"
+        "\"slab_create_us_per_chunk\":%.1f}\n",
         slab, m, live_h.size(), load ? "hbm_stream" : "idle", med(create_us), med(map_us),
-        med(access_us), med(unmap_us), run16);
+        med(access_us), med(unmap_us), run16, slab_us);
     std::fflush(stdout);
   };
   for (int m : {0, 512, 2048, 8192, 16384, 24576}) {
