@@ -222,6 +222,7 @@ def main():
         eng.build_allocator = build
         rep = eng.ServingEngine(cfg, trace, allocator="vtensor", device=dev).run()
         torch.cuda.synchronize()
+        dev.wait()  # the shutdown's unmaps / destroys have run on the driver
         ad = holder["ad"]
         chk = ad.on_step
         logged = {}
