@@ -124,22 +124,23 @@ def bench_decode(args, pk):
             layer = [0]
             km = maps if path == "tcgen05" else None
 
-            def fn():
+            def fn(chained=False):
                 decode_attention(q, kv_va, seq, layer[0] % L, geo, ctx, out=out, workspace=ws,
-                                 split_tokens=split, kv_maps=km)
+                                 split_tokens=split, kv_maps=km, chained=chained)
                 layer[0] += 1  # rotate layers: 1 GiB per launch, never L2-resident
 
             if args.loop:  # 32 back-to-back layer launches, like one decode step
                 def fn32():
-                    for _ in range(L):
-                        fn()
+                    for i in range(L):
+                        fn(chained=args.chained and path == "tcgen05" and i > 0)
                 ms, _ = timed(fn32, max(2, args.iters // 4), args.warmup)
                 ms /= L
             else:
                 ms, _ = timed(fn, args.iters, args.warmup)
             nbytes = 2 * B * ctx * hkv * 128 * 2 + 2 * B * hq * 128 * 2
             gbs = nbytes / (ms * 1e-3) / 1e9
-            res.append({"kernel": f"decode[{path}]" + ("x32" if args.loop else ""),
+            res.append({"kernel": f"decode[{path}]" + ("x32" if args.loop else "")
+                        + ("_pdl" if args.loop and args.chained else ""),
                         "config": f"{args.shape} B64 ctx4096 G={hq // hkv}",
                         "split": split, "us": round(ms * 1e3, 2), "bytes": nbytes,
                         "GB/s": round(gbs, 1), "frac_of_hbm": round(gbs / pk["hbm_gbs"], 4)})
@@ -254,6 +255,8 @@ def main():
     ap.add_argument("--splits", type=lambda s: [int(x) for x in s.split(",")], default=[1024])
     ap.add_argument("--paths", type=lambda s: s.split(","), default=["tcgen05", "cuda_core"])
     ap.add_argument("--loop", action="store_true", help="time 32 back-to-back launches")
+    ap.add_argument("--chained", action="store_true",
+                    help="with --loop: layers after the first use programmatic dependent launch")
     ap.add_argument("--shape", choices=["8b", "70b", "toy", "mha64"], default="8b")
     ap.add_argument("--qkv-batch", type=lambda s: [int(x) for x in s.split(",")], default=[64])
     ap.add_argument("--qkv-split", type=lambda s: [int(x) for x in s.split(",")], default=[0])
