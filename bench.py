@@ -93,6 +93,9 @@ def parse():
                          "the run will create, capped at 16 GiB; 0 = off)")
     ap.add_argument("--driver-threads", type=int, default=0,
                     help="shim threads executing driver VMM ops in parallel (0 = library default)")
+    ap.add_argument("--lead-chunks", type=int, default=0,
+                    help="extend this many chunks ahead of each request's next token (0 = 3 with "
+                         "chained layers, 1 without; the growth trace uses 8)")
     ap.add_argument("--check", action="store_true",
                     help="after the timed region, compare sampled (request, layer) outputs of the "
                          "last step (and the config-3 prefill probe) with the CPU oracle")
@@ -305,7 +308,7 @@ class DecodeWorkload:
     def __init__(self, cfg_name: str, split: int, seed: int, path: str = "tcgen05",
                  world: int = 1, rank: int = 0, premap_steps: int = 0, chain: bool = True,
                  total_steps: int = 64, start_len: int = 0, max_seq: int = 0,
-                 phys_reserve: int = -1, driver_threads: int = 0):
+                 phys_reserve: int = -1, driver_threads: int = 0, lead_chunks: int = 0):
         import torch
 
         import paper_2407_15309_b200 as vt
@@ -333,7 +336,8 @@ class DecodeWorkload:
         # 0.15-2 ms of driver time per chunk (tools/vmm_probe.cu), i.e. a few
         # steps when several requests cross a chunk edge together
         self.chain = chain
-        self.lead_chunks = int(os.environ.get("VT_LEAD_CHUNKS", "3" if chain else "1"))
+        self.lead_chunks = lead_chunks or int(os.environ.get("VT_LEAD_CHUNKS",
+                                                             "3" if chain else "1"))
         win = self.map_ahead * tpc
         self.rids = [f"r{b}" for b in range(B)]
         if start_len:  # growth trace: every request starts at the same length
@@ -568,7 +572,10 @@ def run_ours(args, world, rank, local):
                             chain=not args.no_chain, total_steps=total_steps,
                             start_len=GROWTH_START, max_seq=32768,
                             phys_reserve=0 if args.premap else args.phys_reserve,
-                            driver_threads=args.driver_threads)
+                            driver_threads=args.driver_threads,
+                            # every request crosses a chunk edge every 16 steps for the
+                            # whole trace: cover the driver's tail latency (p99 ~0.2-1 s)
+                            lead_chunks=args.lead_chunks or 8)
     else:
         total_steps = args.warmup + 2 * args.steps + 2
         wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
@@ -576,7 +583,7 @@ def run_ours(args, world, rank, local):
                             premap_steps=total_steps if args.premap else 0,
                             chain=not args.no_chain, total_steps=total_steps,
                             phys_reserve=0 if args.premap else args.phys_reserve,
-                            driver_threads=args.driver_threads)
+                            driver_threads=args.driver_threads, lead_chunks=args.lead_chunks)
     wl.dev.wait()  # the physical reserve (if any) is filled before any timing
     if args.profile_steps:
         for _ in range(args.profile_steps):

@@ -167,10 +167,11 @@ int vt_driver_stats_get(const vt_device* dev, vt_driver_stats* out);
 /* Driver-op parallelism (no reference counterpart: the reference's device is
  * in-process and instantaneous, device.py:118-295). Each queued batch runs
  * as maximal same-kind segments in issue order; the ops of one segment are
- * independent and run on `threads` threads (default 4, env VT_DRIVER_THREADS).
- * On the B200 driver each cuMemCreate / cuMemSetAccess / cuMemUnmap waits
- * 150-720 us (not CPU-bound), so parallel callers multiply the mapping rate
- * (tools/vmm_probe.cu). Blocks until queued work has drained. */
+ * independent and run on `threads` threads (default 1, env VT_DRIVER_THREADS).
+ * Several threads multiply the mapping rate on an idle GPU (tools/vmm_probe.cu)
+ * but, under the decode stream, concurrent map/SetAccess calls serialise in
+ * the driver and starve the launching thread, so serving runs
+ * with one. Blocks until queued work has drained. */
 int vt_set_driver_threads(vt_device* dev, int threads);
 /* Physical-handle reserve: keep up to `chunks` cuMemCreate'd handles that are
  * not (yet) logical chunks. A logical create_chunk takes one from the reserve

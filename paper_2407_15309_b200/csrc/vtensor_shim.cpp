@@ -395,10 +395,10 @@ struct vt_device {
   }
 
   // ---- driver thread pool: parallel_for over independent driver ops ----
-  // Measured on the B200 box (tools/vmm_probe.cu "alternate"): one thread
-  // completes 0.5-1.6 map+SetAccess per ms (each call waits 150-720 us on the
-  // driver, not the CPU), four threads 2-6 per ms, and none of it slows the
-  // HBM-streaming kernels running meanwhile.
+  // On an idle GPU (tools/vmm_probe.cu "alternate") one thread completes
+  // 0.5-1.6 map+SetAccess per ms and four threads 2-6 per ms; under the decode
+  // stream concurrent calls serialise in the driver and block kernel launches,
+  // so the default is one thread (see vt_dev_open).
   // A job is closed only when every item ran AND every pool thread that
   // joined it has left it (job_fn is cleared first, so no thread can join
   // late): a thread still inside run_job_items must never claim an item of
@@ -790,7 +790,13 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
     if (drv.EventCreate(&d->fence_src, CU_EVENT_DISABLE_TIMING) != CUDA_SUCCESS ||
         drv.StreamCreate(&d->fence_stream, CU_STREAM_NON_BLOCKING) != CUDA_SUCCESS)
       return fail_open(VT_E_CUDA);
-    int threads = 4;
+    // One driver thread by default. Measured in the config-2 bench (300 steps,
+    // 1200 chunks mapped under the decode stream, profiles/r02/bench/
+    // cfg2_300_*.json): with 4 threads issuing map + SetAccess concurrently the
+    // calls serialise inside the driver and keep the lock the launching thread
+    // needs (GPU idle 1477 ms, 145 host waits, 3537 GB/s); one thread: 0 host
+    // waits, 6669 GB/s. More threads only pay off for bulk work on an idle GPU.
+    int threads = 1;
     if (const char* e = std::getenv("VT_DRIVER_THREADS")) threads = std::atoi(e);
     d->driver_threads = std::max(1, std::min(threads, 16));
     d->start_pool(d->driver_threads);
