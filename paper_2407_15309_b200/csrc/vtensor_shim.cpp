@@ -239,6 +239,7 @@ struct vt_device {
   int job_active = 0;  // pool threads inside the current job (guarded by pool_mu)
   std::atomic<size_t> job_next{0}, job_left{0};
   int driver_threads = 1;
+  bool setaccess_runs = false;  // one cuMemSetAccess per contiguous run of maps (VT_SETACCESS_RUNS=1)
   std::mutex lat_mu;
   std::vector<int64_t> lat[6];  // per vt_op: submit -> completed, ns
 
@@ -511,6 +512,39 @@ struct vt_device {
     dstats.access_ns_total += t1 - ta;
     dstats.map_ns_total += t1 - t0;
   }
+  // A run of maps onto consecutive pages: one cuMemMap per chunk (every chunk
+  // is its own allocation), then ONE cuMemSetAccess over the whole run.
+  void do_map_run(const DrvOp* ops, size_t n) {
+    Driver& d = driver();
+    const size_t len = static_cast<size_t>(cfg.chunk_bytes);
+    int64_t t0 = now_ns();
+    size_t mapped = 0;
+    for (; mapped < n; ++mapped) {
+      bool found = false;
+      CUmemGenericAllocationHandle h = phys_get(ops[mapped].handle_id, &found);
+      if (!found) {
+        record_error("map of a chunk the driver never created (id " +
+                     std::to_string(ops[mapped].handle_id) + ")");
+        break;
+      }
+      CUresult r = d.MemMap(ops[mapped].addr, len, 0, h, 0);
+      if (r != CUDA_SUCCESS) {
+        record_error("cuMemMap: " + cu_err(r));
+        break;
+      }
+    }
+    int64_t ta = now_ns();
+    if (mapped) {
+      CUresult r = d.MemSetAccess(ops[0].addr, len * mapped, &access, 1);
+      if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
+    }
+    int64_t t1 = now_ns();
+    std::lock_guard<std::mutex> lk(stat_mu);
+    dstats.map_calls += static_cast<int64_t>(mapped);
+    dstats.access_calls++;
+    dstats.access_ns_total += t1 - ta;
+    dstats.map_ns_total += t1 - t0;
+  }
   void do_unmap(const DrvOp& op) {
     int64_t t0 = now_ns();
     CUresult r = driver().MemUnmap(op.addr, static_cast<size_t>(cfg.chunk_bytes));
@@ -581,7 +615,19 @@ struct vt_device {
           parallel_for(m, [&](size_t k) { do_create(seg[k]); });
           break;
         case DrvKind::kMap:
-          parallel_for(m, [&](size_t k) { do_map_one(seg[k]); });
+          if (setaccess_runs) {
+            // contiguous runs (an extend maps consecutive pages of one space)
+            std::vector<std::pair<size_t, size_t>> runs;
+            for (size_t k = 0; k < m; ++k) {
+              if (!runs.empty() && seg[k].addr == seg[k - 1].addr + static_cast<CUdeviceptr>(cfg.chunk_bytes))
+                runs.back().second++;
+              else
+                runs.push_back({k, 1});
+            }
+            parallel_for(runs.size(), [&](size_t r) { do_map_run(seg + runs[r].first, runs[r].second); });
+          } else {
+            parallel_for(m, [&](size_t k) { do_map_one(seg[k]); });
+          }
           break;
         case DrvKind::kUnmap:
           parallel_for(m, [&](size_t k) { do_unmap(seg[k]); });
@@ -799,6 +845,7 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
     int threads = 1;
     if (const char* e = std::getenv("VT_DRIVER_THREADS")) threads = std::atoi(e);
     d->driver_threads = std::max(1, std::min(threads, 16));
+    if (const char* e = std::getenv("VT_SETACCESS_RUNS")) d->setaccess_runs = std::atoi(e) != 0;
     d->start_pool(d->driver_threads);
     d->worker = std::thread([d] { d->worker_main(); });
   }
