@@ -140,6 +140,17 @@ int vt_map_pages(vt_device* dev, int64_t base, int64_t first_page,
 int vt_unmap_tail(vt_device* dev, int64_t base, int64_t from_page_inclusive,
                   int64_t down_to_inclusive, int64_t* handle_ids_out, int64_t* n_done);
 
+/* One scheduler extend in one call (scheduler.py:166-180: ops.py:83-112 p_alloc
+ * then ops.py:133-146 map_chunks): creates n_create chunks (ids written to
+ * created_ids), then maps the n_reuse parked handles followed by the created
+ * ones at pages first_page.. of the range. Call log = create_chunk x n_create,
+ * then map_page per page, exactly as the two-op sequence; the driver work is
+ * queued with one worker wake-up. All-or-nothing: on any error nothing
+ * changed (the caller then runs the per-op sequence, which reproduces the
+ * reference's partial-failure behaviour). */
+int vt_extend(vt_device* dev, int64_t base, int64_t first_page, const int64_t* reuse_ids,
+              int64_t n_reuse, int64_t n_create, int64_t* created_ids);
+
 /* ---- accounting / inspection (device.py:141-187, 272-295) ---------------- */
 int vt_set_active_requests(vt_device* dev, int64_t n);
 int vt_get_stats(const vt_device* dev, vt_stats* out);

@@ -135,6 +135,7 @@ def vtensor_lib() -> ctypes.CDLL:
         "vt_chunk_is_imported": (c_int, [c_void_p, c_int64]),
         "vt_map_pages": (c_int, [c_void_p, c_int64, c_int64, P64, c_int64, P64]),
         "vt_unmap_tail": (c_int, [c_void_p, c_int64, c_int64, c_int64, P64, P64]),
+        "vt_extend": (c_int, [c_void_p, c_int64, c_int64, P64, c_int64, c_int64, P64]),
         "vt_set_active_requests": (c_int, [c_void_p, c_int64]),
         "vt_get_stats": (c_int, [c_void_p, POINTER(VtStats)]),
         "vt_resolve": (c_int, [c_void_p, c_int64, c_int64, P64]),
@@ -168,10 +169,19 @@ def vtensor_lib() -> ctypes.CDLL:
     return lib
 
 
+def vtfast():
+    """The CPython fast-call module for the manager's hot shim calls
+    (csrc/vt_pyfast.c); its symbols bind to the libvtensor.so loaded above."""
+    vtensor_lib()
+    from . import _vtfast
+
+    return _vtfast
+
+
 VTENSOR_SYMBOLS = (
     "vt_dev_open", "vt_dev_close", "vt_dev_is_cuda", "vt_last_error",
     "vt_reserve", "vt_create_chunk", "vt_map_page", "vt_unmap_page",
-    "vt_release", "vt_destroy_chunk", "vt_map_pages", "vt_unmap_tail",
+    "vt_release", "vt_destroy_chunk", "vt_map_pages", "vt_unmap_tail", "vt_extend",
     "vt_set_active_requests", "vt_get_stats", "vt_resolve", "vt_handle_alive",
     "vt_live_handles", "vt_live_ranges", "vt_range_mappings",
     "vt_call_log_len", "vt_call_log_read", "vt_ticket", "vt_wait", "vt_poll",

@@ -2,6 +2,9 @@
 to the GPU box with the repo snapshot).
 
   libvtensor.so : g++ -O2, C++17, dlopens libcuda at run time (include/vtensor.h)
+  _vtfast*.so   : gcc -O2, CPython entry points for the manager's per-token
+                  calls into libvtensor.so (symbols resolved from the
+                  RTLD_GLOBAL-loaded shim, so an A/B shim build is honoured)
   libvtattn.so  : nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo
                   (include/vt_attention.h)
 """
@@ -40,6 +43,13 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
     if force or _stale(shim, shim_src + hdrs):
         _run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-Wall", f"-I{CUDA}/include",
               "-o", shim, *shim_src, "-ldl", "-lpthread"])
+    import sysconfig
+
+    fast_src = [os.path.join(CSRC, "vt_pyfast.c")]
+    fast = os.path.join(PKG, "_vtfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if force or _stale(fast, fast_src + hdrs):
+        _run(["gcc", "-O2", "-fPIC", "-shared", "-Wall", f"-I{sysconfig.get_paths()['include']}",
+              "-o", fast, *fast_src])
     cu_src = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     attn = os.path.join(PKG, "libvtattn.so")
     if force or _stale(attn, cu_src + hdrs):

@@ -961,6 +961,60 @@ int vt_map_pages(vt_device* d, int64_t base, int64_t first_page, const int64_t* 
   return rc;
 }
 
+// One scheduler extend (scheduler.py:166-180 = ops.py:83-112 p_alloc followed by
+// ops.py:133-146 map_chunks) in one crossing: n_create chunks created, then the
+// n_reuse parked handles and the created ones mapped at consecutive pages from
+// first_page. The call log equals create_chunk x n_create, then map_page per
+// page, and the driver work is queued with one wake-up. All-or-nothing: every
+// precondition (budget, range, free slots, live reused handles) is checked
+// before any state changes; on failure nothing happened and the caller takes
+// the per-op path, which reproduces the reference's partial behaviour.
+int vt_extend(vt_device* d, int64_t base, int64_t first_page, const int64_t* reuse_ids,
+              int64_t n_reuse, int64_t n_create, int64_t* created_ids) {
+  if (n_reuse < 0 || n_create < 0)
+    return d->fail(VT_E_INDEX_OUT_OF_RANGE, "negative chunk count");
+  if (n_create > 0 && d->free_bytes() < n_create * d->cfg.chunk_bytes)
+    return d->fail(VT_E_OUT_OF_MEMORY,
+                   "need " + std::to_string(n_create * d->cfg.chunk_bytes) + " bytes, " +
+                       std::to_string(d->free_bytes()) + " free");
+  auto it = d->ranges.find(base);
+  if (it == d->ranges.end())
+    return d->fail(VT_E_UNKNOWN_RANGE, "range base " + std::to_string(base) + " is not reserved");
+  RangeState& rs = it->second;
+  const int64_t n = n_reuse + n_create;
+  if (first_page < 0 || first_page + n > rs.pages)
+    return d->fail(VT_E_INDEX_OUT_OF_RANGE, "pages " + std::to_string(first_page) + ".." +
+                                                std::to_string(first_page + n - 1) +
+                                                " outside range of " + std::to_string(rs.pages) +
+                                                " pages");
+  for (int64_t k = 0; k < n; ++k)
+    if (rs.slot[static_cast<size_t>(first_page + k)] >= 0)
+      return d->fail(VT_E_PAGE_ALREADY_MAPPED, "page " + std::to_string(first_page + k) +
+                                                   " of base " + std::to_string(base) +
+                                                   " is mapped");
+  for (int64_t k = 0; k < n_reuse; ++k)
+    if (d->handles.find(reuse_ids[k]) == d->handles.end())
+      return d->fail(VT_E_STALE_HANDLE, "handle " + std::to_string(reuse_ids[k]) +
+                                            " was destroyed or never created");
+  for (int64_t k = 0; k < n_create; ++k) {
+    const int64_t h = d->next_handle++;
+    d->handles.emplace(h, 0);
+    d->log_call(VT_OP_CREATE_CHUNK, 0, 0, h, 0);
+    if (d->is_cuda()) {
+      DrvOp op{};
+      op.kind = DrvKind::kCreate;
+      op.handle_id = h;
+      d->enqueue(op);
+    }
+    created_ids[k] = h;
+  }
+  int rc = VT_OK;
+  for (int64_t k = 0; k < n && rc == VT_OK; ++k)
+    rc = do_map(d, base, first_page + k, k < n_reuse ? reuse_ids[k] : created_ids[k - n_reuse]);
+  d->kick();
+  return rc;  // VT_OK: the checks above leave do_map nothing to reject
+}
+
 // device.py:235-245
 int vt_unmap_page(vt_device* d, int64_t base, int64_t page, int64_t* id) {
   int rc = do_unmap(d, base, page, id);

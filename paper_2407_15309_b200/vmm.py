@@ -212,6 +212,7 @@ class VirtualMemoryDevice:
     def __init__(self, config: DeviceConfig, cuda_ordinal: int | None = None) -> None:
         self.config = config
         self._lib = N.vtensor_lib()
+        self._fast = N.vtfast()
         cfg = N.VtConfig(
             config.capacity_bytes,
             config.chunk_size_bytes,
@@ -233,11 +234,13 @@ class VirtualMemoryDevice:
         self._log_len = 0
         self._i64 = ctypes.c_int64()
         self._i64b = ctypes.c_int64()
+        self._hv = handle.value  # the vt_device* as an int, for the fast-call module
 
     # -- lifetime -------------------------------------------------------------
 
     def close(self) -> None:
         if getattr(self, "_h", None):
+            self._hv = 0
             self._lib.vt_dev_close(self._h)
             self._h = None
 
@@ -341,6 +344,27 @@ class VirtualMemoryDevice:
         if rc:
             self._raise(rc, done)
 
+    def extend_pages(self, rng: VirtualRange, first_page: int, reused: list[PhysicalHandle],
+                     n_create: int) -> list[PhysicalHandle] | None:
+        """``create_chunk`` x n_create then ``map_pages(reused + created)`` in one
+        shim call (``vt_extend``; same call log). All-or-nothing: returns None,
+        with nothing changed, when any precondition fails — the caller then
+        runs the per-op sequence, which raises exactly as the reference does."""
+        ids = self._fast.extend(self._hv, rng.base, first_page, [h.id for h in reused], n_create)
+        if ids is None:
+            return None
+        interned = self._interned
+        fresh = []
+        for hid in ids:
+            h = PhysicalHandle(id=hid)
+            interned[hid] = h
+            fresh.append(h)
+        handles = reused + fresh if reused else fresh
+        for h in handles:
+            h.map_count += 1
+        self._log_len += n_create + len(handles)
+        return handles
+
     def unmap_page(self, rng: VirtualRange, page_index: int) -> PhysicalHandle:
         rc = self._lib.vt_unmap_page(self._h, rng.base, page_index, ctypes.byref(self._i64))
         if rc:
@@ -355,14 +379,13 @@ class VirtualMemoryDevice:
         n = from_page - down_to + 1
         if n <= 0:
             return []
-        ids = (ctypes.c_int64 * n)()
-        rc = self._lib.vt_unmap_tail(self._h, rng.base, from_page, down_to, ids,
-                                     ctypes.byref(self._i64))
-        out = []
-        done = self._i64.value
+        rc, ids = self._fast.unmap_tail(self._hv, rng.base, from_page, down_to)
+        done = len(ids)
         self._log_len += done
-        for i in range(done):
-            h = self._interned[ids[i]]
+        interned = self._interned
+        out = []
+        for hid in ids:
+            h = interned[hid]
             h.map_count -= 1
             out.append(h)
         if rc:

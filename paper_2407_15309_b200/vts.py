@@ -161,7 +161,7 @@ class VTensorScheduler:
         deficit = _ceil_div(target_tokens, self.config.tokens_per_chunk) - rm.vt.space.mapped_pages
         if deficit <= 0:
             return 0
-        self.ops.map_chunks(rm.vt.space, self.ops.p_alloc(deficit))
+        self.ops.extend_space(rm.vt.space, deficit)  # p_alloc + map_chunks, one shim call
         return deficit
 
     def mark_prefilled(self, request_id: str) -> None:
