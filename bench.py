@@ -96,6 +96,13 @@ def parse():
     ap.add_argument("--lead-chunks", type=int, default=0,
                     help="extend this many chunks ahead of each request's next token (0 = 3 with "
                          "chained layers, 1 without; the growth trace uses 8)")
+    ap.add_argument("--plain-every", type=int, default=0,
+                    help="with chained decode layers, also launch every N-th layer of a run "
+                         "plainly (a kernel boundary where queued cuMemMap/cuMemSetAccess "
+                         "complete); 0 = only the run's first layer")
+    ap.add_argument("--plain-adaptive", action="store_true",
+                    help="apply --plain-every only to steps enqueued while the shim's driver "
+                         "worker still has mapping work outstanding")
     ap.add_argument("--check", action="store_true",
                     help="after the timed region, compare sampled (request, layer) outputs of the "
                          "last step (and the config-3 prefill probe) with the CPU oracle")
@@ -363,6 +370,9 @@ class DecodeWorkload:
         self.host_waits = 0
         self.host_wait_ns = 0
         self.chained_steps = 0
+        self.plain_every = 0  # see --plain-every
+        self.plain_adaptive = False
+        self.boundaries = 0  # plain decode launches (kernel boundaries) enqueued
         self.last_done = None
         self.gap_events: list | None = None  # (previous step's end, this step's start)
         self.extend_ns: list[int] = []
@@ -484,6 +494,9 @@ class DecodeWorkload:
         # issued `lead_chunks` chunks ahead (0 host waits, 0 stalls measured).
         chain = self.chain
         self.chained_steps += int(chain)
+        pe = self.plain_every
+        if pe and self.plain_adaptive and self.dev.ready(self.dev.ticket()):
+            pe = 0  # nothing queued on the driver worker: keep the whole chain
         torch.add(self.seq, 1, out=self.seq1)  # lengths including this step's token
         for gi, grp in enumerate(self.groups):
             kv_maps = None
@@ -503,9 +516,11 @@ class DecodeWorkload:
                 run_events[gi][0].record(self.stream)
             for li in range(grp.n_layers):
                 layer = lo + li
+                chained = chain and li > 0 and not (pe and li % pe == 0)
+                self.boundaries += not chained
                 decode_attention(q[layer], grp.kv_va, self.seq1, li, grp.geo, mx,
                                  out=out[layer], workspace=self.ws, split_tokens=self.split,
-                                 kv_maps=kv_maps, chained=chain and li > 0)
+                                 kv_maps=kv_maps, chained=chained)
                 launches += last_launches()
             if run_events is not None:
                 run_events[gi][1].record(self.stream)
@@ -584,6 +599,7 @@ def run_ours(args, world, rank, local):
                             chain=not args.no_chain, total_steps=total_steps,
                             phys_reserve=0 if args.premap else args.phys_reserve,
                             driver_threads=args.driver_threads, lead_chunks=args.lead_chunks)
+    wl.plain_every, wl.plain_adaptive = args.plain_every, args.plain_adaptive
     wl.dev.wait()  # the physical reserve (if any) is filled before any timing
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -607,6 +623,7 @@ def run_ours(args, world, rank, local):
     waits0 = wl.host_waits
     wait_ns0 = wl.host_wait_ns
     chained0 = wl.chained_steps
+    bounds0 = wl.boundaries
     drv0 = wl.dev.driver_stats()
     wl.dev.driver_latencies("map_page", reset=True)
     wl.extend_ns.clear()
@@ -636,6 +653,7 @@ def run_ours(args, world, rank, local):
     n_decode = wl.L * args.steps  # decode launches inside the bracketed runs
     stalls = wl.stalls - stalls0
     chained = wl.chained_steps - chained0
+    plain_per_step = (wl.boundaries - bounds0) / max(args.steps, 1)
     elapsed_max = max_over_ranks(elapsed_ms, world)
     bytes_all = sum_over_ranks(bytes_total, world)
     tokens_all = wl.B * args.steps * (1 if wl.head_partition else world)
@@ -790,6 +808,9 @@ def run_ours(args, world, rank, local):
                 "gpu_idle_gap_ms_max": round(max(gaps), 3) if gaps else 0.0,
                 "host_wait_ms_total": round((wl.host_wait_ns - wait_ns0) / 1e6, 3),
                 "chained_steps": chained,
+                "plain_decode_launches_per_step": round(plain_per_step, 2),
+                "plain_every": args.plain_every,
+                "plain_adaptive": args.plain_adaptive,
                 "lead_chunks": wl.lead_chunks,
                 "ready_note": ("chained layers leave the driver one plain kernel boundary per "
                                "step, where cuMemMap/cuMemSetAccess complete: ready latency is "
