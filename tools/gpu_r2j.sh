@@ -20,5 +20,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:pref
   -o $O/prefill python tools/kernel_bench.py --which prefill --iters 1 --warmup 3 > $O/prefill.log 2>&1; echo "ncu prefill rc=$?" >> $O/status
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:qkv_append -s 6 -c 1 \
   -o $O/qkv python tools/kernel_bench.py --which qkv > $O/qkv.log 2>&1; echo "ncu qkv rc=$?" >> $O/status
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"vt::|kv_append|decode|prefill|qkv" -c 300 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/launches.log 2>&1; echo "launches rc=$?" >> $O/status
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"kv_append|decode|prefill|qkv|combine" -c 300 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/launches.log 2>&1; echo "launches rc=$?" >> $O/status
 cat $O/status
