@@ -58,3 +58,28 @@ def test_attention_rejects_cpu_tensors():
 
     with pytest.raises(RuntimeError):
         _need_cuda(torch.zeros(4))
+
+
+def test_fused_extend_is_all_or_nothing_and_logs_like_the_two_ops():
+    """vt_extend (one scheduler extend = p_alloc creates + map_chunks maps in
+    one shim call): the call log equals create_chunk x n then map_page per
+    page, and a rejected call (budget, occupied page) changes nothing."""
+    import paper_2407_15309_b200 as vt
+
+    dev = vt.VirtualMemoryDevice(vt.DeviceConfig(capacity_bytes=8 << 21, chunk_size_bytes=2 << 20))
+    rng = dev.reserve_address(6 << 21)
+    parked = dev.create_chunk()
+    got = dev.extend_pages(rng, 0, [parked], 2)
+    assert [h.id for h in got] == [parked.id, parked.id + 1, parked.id + 2]
+    assert [c.op for c in dev.call_log] == ["reserve_address", "create_chunk", "create_chunk",
+                                            "create_chunk", "map_page", "map_page", "map_page"]
+    assert all(h.map_count == 1 for h in got)
+    n = len(dev.call_log)
+    stats = dev.stats()
+    assert dev.extend_pages(rng, 2, [], 1) is None  # page 2 is mapped
+    assert dev.extend_pages(rng, 3, [], 6) is None  # over the 8-chunk budget
+    assert dev.extend_pages(rng, 5, [], 2) is None  # past the range's 6 pages
+    assert len(dev.call_log) == n and dev._lib.vt_call_log_len(dev._h) == n
+    assert dev.stats() == stats
+    assert [h.id for h in dev.extend_pages(rng, 3, [], 3)] == [parked.id + 3, parked.id + 4,
+                                                                parked.id + 5]
