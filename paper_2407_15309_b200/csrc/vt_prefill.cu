@@ -57,7 +57,7 @@ namespace pf {
 constexpr int BM = 128;  // query rows per slot
 constexpr int BN = 128;  // keys per K/V tile and per score block
 constexpr int D = 128;
-constexpr int kRing = 3;  // K/V tiles in one ring, consumed K0, then K(j+1), V(j) per block
+constexpr int kStages = 2;
 constexpr int kSlots = 2;
 constexpr int kThreads = kSlots * 128 + 128;  // softmax WGs, then TMA/MMA WG
 constexpr uint32_t kTmemCols = 512;
@@ -73,14 +73,14 @@ constexpr uint32_t kPolyMask = VT_PF_POLY_MASK;
 
 struct __align__(1024) Smem {
   __nv_bfloat16 q[kSlots][2][BM * 64];    // SW128 K-major: d 0-63 | d 64-127
-  __nv_bfloat16 kv[kRing][2][BN * 64];    // K: SW128 K-major (keys x d); V: read as MN-major B
-  __nv_bfloat16 p[kSlots][2][BM * 64];    // P (bf16), SW128 K-major A: keys 0-63 | 64-127
+  __nv_bfloat16 k[kStages][2][BN * 64];   // SW128 K-major (keys x d)
+  __nv_bfloat16 v[kStages][2][BN * 64];   // SW128, read as MN-major B (d x keys)
   uint64_t q_full, q_empty;
-  uint64_t kv_full[kRing], kv_empty[kRing];
-  uint64_t s_full[kSlots];     // S of the slot's current block is in TMEM
-  uint64_t s_free[kSlots];     // the softmax has S in registers: S(j+1) may overwrite it
-  uint64_t p_full[kSlots][2];  // P of keys 0-63 / 64-127 of the block is in shared memory
-  uint64_t o_done[kSlots];     // the slot's PV of the block completed (O updated, P free)
+  uint64_t k_full[kStages], k_empty[kStages];
+  uint64_t v_full[kStages], v_empty[kStages];
+  uint64_t s_full[kSlots];
+  uint64_t p_full[kSlots][2];  // P of keys 0-63 / 64-127 of the block is in TMEM
+  uint64_t o_done[kSlots];
   uint32_t tmem_base;
 };
 
@@ -215,13 +215,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kTmaWarp && lane == 0) {
     mbar_init(&sm.q_full, 1);
     mbar_init(&sm.q_empty, 1);
-    for (int i = 0; i < kRing; ++i) {
-      mbar_init(&sm.kv_full[i], 1);
-      mbar_init(&sm.kv_empty[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.k_full[i], 1);
+      mbar_init(&sm.k_empty[i], 1);
+      mbar_init(&sm.v_full[i], 1);
+      mbar_init(&sm.v_empty[i], 1);
     }
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&sm.s_full[s], 1);
-      mbar_init(&sm.s_free[s], 128);
       mbar_init(&sm.p_full[s][0], 128);
       mbar_init(&sm.p_full[s][1], 128);
       mbar_init(&sm.o_done[s], 1);
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&q_map);
         const uint64_t keep = l2_evict_last_policy();   // K/V re-read by the group's heads
         const uint64_t once = l2_evict_first_policy();
-        int u = 0;  // ring tiles loaded so far
+        int g = 0;  // K/V tiles loaded so far
         int n = 0;  // items so far
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
           const Item it = item_of(w, a);
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_prefetch_l2_4d(&q_map, 64, nx.h0 + s, nx.q0 + nx.t * BM, 0);
             }
             const CUtensorMap* nmap = a.kv + nx.b;
-            for (int j = 0; j < min(nx.n_kv, 2); ++j) {
+            for (int j = 0; j < min(nx.n_kv, kStages); ++j) {
               const int tok0 = j * BN;
               tma_prefetch_l2_4d(nmap, 0, tok0 % a.tpc, nx.blk_k, tok0 / a.tpc);
               tma_prefetch_l2_4d(nmap, 64, tok0 % a.tpc, nx.blk_k, tok0 / a.tpc);
@@ -275,31 +276,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_prefetch_l2_4d(nmap, 64, tok0 % a.tpc, nx.blk_v, tok0 / a.tpc);
             }
           }
-          // Ring order = consumption order: K(0), then per block j: K(j+1)
-          // (S(j+1) is issued as soon as the softmax holds S(j)), V(j).
-          for (int i = 0; i < 2 * it.n_kv; ++i, ++u) {
-            bool is_k;
-            int blk;
-            if (i == 0) {
-              is_k = true;
-              blk = 0;
-            } else if (i & 1) {
-              const int j = (i - 1) >> 1;
-              is_k = j + 1 < it.n_kv;
-              blk = is_k ? j + 1 : j;
-            } else {
-              is_k = false;
-              blk = (i - 2) >> 1;
-            }
-            const int st = u % kRing;
-            const int tok0 = blk * BN;
+          for (int j = 0; j < it.n_kv; ++j, ++g) {
+            const int st = g % kStages;
+            const uint32_t ph = (g / kStages) & 1;
+            const int tok0 = j * BN;
             const int c1 = tok0 % a.tpc;
             const int c3 = tok0 / a.tpc;
-            const int cb = is_k ? it.blk_k : it.blk_v;
-            if (u >= kRing) mbar_wait(&sm.kv_empty[st], ((u / kRing) & 1) ^ 1);
-            mbar_arrive_expect_tx(&sm.kv_full[st], 2 * BN * 64 * 2);
-            tma_load_4d(sm.kv[st][0], kvmap, &sm.kv_full[st], 0, c1, cb, c3, keep);
-            tma_load_4d(sm.kv[st][1], kvmap, &sm.kv_full[st], 64, c1, cb, c3, keep);
+            if (g >= kStages) mbar_wait(&sm.k_empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&sm.k_full[st], 2 * BN * 64 * 2);
+            tma_load_4d(sm.k[st][0], kvmap, &sm.k_full[st], 0, c1, it.blk_k, c3, keep);
+            tma_load_4d(sm.k[st][1], kvmap, &sm.k_full[st], 64, c1, it.blk_k, c3, keep);
+            if (g >= kStages) mbar_wait(&sm.v_empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&sm.v_full[st], 2 * BN * 64 * 2);
+            tma_load_4d(sm.v[st][0], kvmap, &sm.v_full[st], 0, c1, it.blk_v, c3, keep);
+            tma_load_4d(sm.v[st][1], kvmap, &sm.v_full[st], 64, c1, it.blk_v, c3, keep);
           }
           ++n;
         }
@@ -312,17 +302,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t hi = tc::sdesc_hi(1024);  // SW128: 8-row groups 1 KiB apart
       // Descriptor address fields count 16 B units: a [.][64] bf16 tile half
       // is 16 KiB = 1024 units, one 16-element K step inside a SW128 row = 2,
-      // 16 keys of V = 128, one ring stage / slot = 2048.
+      // 16 keys of V = 128.
       const uint32_t lq = tc::sdesc_lo(smem_u32(sm.q[0][0]), 16);
-      const uint32_t lp = tc::sdesc_lo(smem_u32(sm.p[0][0]), 16);
-      const uint32_t lk = tc::sdesc_lo(smem_u32(sm.kv[0][0]), 16);
-      const uint32_t lv = tc::sdesc_lo(smem_u32(sm.kv[0][0]), BN * 128);
+      const uint32_t lk = tc::sdesc_lo(smem_u32(sm.k[0][0]), 16);
+      const uint32_t lv = tc::sdesc_lo(smem_u32(sm.v[0][0]), BN * 128);
       auto wait_fence = [&](uint64_t* bar, uint32_t parity) {
         mbar_wait(bar, parity);
         tc::fence_after();
       };
-      auto mma_s = [&](int s, int st) {  // elected lane only; st = ring stage of K
-        const uint32_t b0 = lk + static_cast<uint32_t>(st * 2048);
+      auto mma_s = [&](int s, int g) {  // elected lane only; g = global tile index
+        const uint32_t b0 = lk + static_cast<uint32_t>((g % kStages) * 2048);
         const uint32_t a0 = lq + static_cast<uint32_t>(s * 2048);
         const uint32_t d = tmem + static_cast<uint32_t>(s * BN);
 #pragma unroll
@@ -332,83 +321,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::commit(&sm.s_full[s]);
       };
-      // O += P V over keys [64 hf, 64 hf + 64) of the block (4 MMAs of K16),
-      // P from shared memory: the softmax hands it over in two halves so the
-      // first half's MMAs run while it still exponentiates the second.
-      auto mma_pv_half = [&](int s, int st, int hf, bool first) {  // elected lane only
-        const uint32_t b0 = lv + static_cast<uint32_t>(st * 2048);
-        const uint32_t a0 = lp + static_cast<uint32_t>(s * 2048 + hf * 1024);
+      // O += P V over keys [64 hf, 64 hf + 64) of the block (4 MMAs of K16):
+      // the softmax hands P over in two halves so the first half's MMAs run
+      // while it still exponentiates the second.
+      auto mma_pv_half = [&](int s, int g, int hf, bool first) {  // elected lane only
+        const uint32_t b0 = lv + static_cast<uint32_t>((g % kStages) * 2048);
         const uint32_t d = tmem + kOCol + static_cast<uint32_t>(s * D);
+        const uint32_t p = tmem + static_cast<uint32_t>(s * BN);
 #pragma unroll
         for (int k4 = 0; k4 < BN / 32; ++k4) {
           const int kk = hf * (BN / 32) + k4;
-          tc::mma_ss(d, a0 + static_cast<uint32_t>(2 * k4), hi, b0 + static_cast<uint32_t>(kk * 128),
-                     hi, id_pv, (!first || kk > 0) ? 1u : 0u);
+          tc::mma_ts(d, p + 8 * kk, b0 + static_cast<uint32_t>(kk * 128), hi, id_pv,
+                     (!first || kk > 0) ? 1u : 0u);
         }
+        if (hf == 1) tc::commit(&sm.o_done[s]);
       };
-      int u = 0, g = 0, n = 0;
+      int g = 0, n = 0;
       for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
         const Item it = item_of(w, a);
         if (!it.valid) continue;
         const int n_kv = it.n_kv;
-        const int u0 = u;
-        // S(0) of every slot; its S buffer was last read (into registers) by
-        // the previous item's final softmax before its P arrived.
+        // S(0) of every slot; its S buffer was last read by the previous
+        // item's final PV, issued before (in-order).
         wait_fence(&sm.q_full, n & 1);
-        wait_fence(&sm.kv_full[u0 % kRing], (u0 / kRing) & 1);
+        wait_fence(&sm.k_full[g % kStages], (g / kStages) & 1);
         if (tc::elect_one()) {
 #pragma unroll
           for (int s = 0; s < kSlots; ++s)
-            if (s < nslots) mma_s(s, u0 % kRing);
-          tc::commit(&sm.kv_empty[u0 % kRing]);
+            if (s < nslots) mma_s(s, g);
+          tc::commit(&sm.k_empty[g % kStages]);
           if (n_kv == 1) tc::commit(&sm.q_empty);
         }
         __syncwarp();
         for (int j = 0; j < n_kv; ++j, ++g) {
           const bool more = j + 1 < n_kv;
-          if (more) {
-            // S(j+1) as soon as each slot's softmax holds S(j) in registers:
-            // the tensor pipe computes the next scores while the softmax
-            // exponentiates, instead of after P(j) has been consumed.
-            const int uk = u0 + 2 * j + 1;
-            wait_fence(&sm.kv_full[uk % kRing], (uk / kRing) & 1);
+          mbar_wait(&sm.v_full[g % kStages], (g / kStages) & 1);
+          if (more) mbar_wait(&sm.k_full[(g + 1) % kStages], ((g + 1) / kStages) & 1);
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s) {
-              if (s < nslots) {
-                wait_fence(&sm.s_free[s], g & 1);
-                if (tc::elect_one()) {
-                  mma_s(s, uk % kRing);
-                  if (s == nslots - 1) {
-                    tc::commit(&sm.kv_empty[uk % kRing]);
+          for (int s = 0; s < kSlots; ++s) {
+            if (s < nslots) {
+              const bool last_slot = s == nslots - 1;
+              wait_fence(&sm.p_full[s][0], g & 1);
+              if (tc::elect_one()) mma_pv_half(s, g, 0, j == 0);
+              __syncwarp();
+              wait_fence(&sm.p_full[s][1], g & 1);
+              VT_TRACE(lane == 0, g, 4 + s);
+              if (tc::elect_one()) {
+                mma_pv_half(s, g, 1, j == 0);
+                if (last_slot) tc::commit(&sm.v_empty[g % kStages]);
+                if (more) {
+                  mma_s(s, g + 1);
+                  if (last_slot) {
+                    tc::commit(&sm.k_empty[(g + 1) % kStages]);
                     if (j + 2 == n_kv) tc::commit(&sm.q_empty);  // the item's last S
                   }
                 }
-                __syncwarp();
               }
-            }
-          }
-          const int uv = u0 + 2 * j + (more ? 2 : 1);
-          wait_fence(&sm.kv_full[uv % kRing], (uv / kRing) & 1);
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll
-            for (int s = 0; s < kSlots; ++s) {
-              if (s < nslots) {
-                wait_fence(&sm.p_full[s][hf], g & 1);
-                VT_TRACE(lane == 0 && hf == 1, g, 4 + s);
-                if (tc::elect_one()) {
-                  mma_pv_half(s, uv % kRing, hf, j == 0);
-                  if (hf == 1) {
-                    tc::commit(&sm.o_done[s]);
-                    if (s == nslots - 1) tc::commit(&sm.kv_empty[uv % kRing]);
-                  }
-                }
-                __syncwarp();
-              }
+              __syncwarp();
             }
           }
         }
-        u = u0 + 2 * n_kv;
         ++n;
       }
     }
@@ -422,19 +394,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t s_addr = lane_addr + static_cast<uint32_t>(s * BN);
       const uint32_t o_addr = lane_addr + kOCol + static_cast<uint32_t>(s * D);
-      // This row of P in the SW128 K-major tile: 8-row groups 1 KiB apart,
-      // rows 128 B apart, 16-byte chunk c stored at c ^ (row % 8).
-      const uint32_t p_row = smem_u32(sm.p[s][0]) + static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128);
       const float sl2 = a.scale_log2;
       int g = 0;  // key blocks processed so far (barrier phases)
-      int u = 0;  // ring tiles consumed so far (V stage of a block)
       for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
         const Item it = item_of(w, a);
         if (!it.valid) continue;
         const int qpos = it.start + it.t * BM + row;  // absolute position of this query row
         const int qmin = it.start + it.t * BM;        // smallest query position of the tile
-        const int u0 = u;
-        u += 2 * it.n_kv;
         float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < it.n_kv; ++j, ++g) {
           const int kpos0 = j * BN;
@@ -450,8 +416,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < BN; ++k) x[k] = __uint_as_float(r[k]);
           }
-          tc::fence_before();
-          mbar_arrive(&sm.s_free[s]);  // S(j+1) may now overwrite this slot's S columns
           VT_SUB(row == 0 && s == 0, g, 0);
           if (kpos0 + BN - 1 > qmin || kpos0 + BN > it.kv_len) {
             const int lim = min(qpos + 1, it.kv_len) - kpos0;  // keys [0, lim) are visible
@@ -467,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 16; k < BN; k += 16)
 #pragma unroll
-              for (int u8 = 0; u8 < 8; ++u8) m8[u8] = fmaxf(m8[u8], fmaxf(x[k + u8], x[k + 8 + u8]));
+              for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(x[k + u], x[k + 8 + u]));
             mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                        fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
           }
@@ -480,7 +444,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 sl2v = make_float2(sl2, sl2);
           const float2 negm = make_float2(-m_use, -m_use);
           if (j >= 1 && __any_sync(0xffffffffu, grow)) {
-            // Lazy rescale of O before any of this block's PV: wait for PV(j-1).
+            // Lazy rescale of O before any of this block's PV: PV(j-1) is
+            // complete (S(j), issued after it, has completed).
             mbar_wait(&sm.o_done[s], (g - 1) & 1);
             tc::fence_after();
 #pragma unroll
@@ -492,31 +457,31 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
               tmem_st32(o_addr + 32 * c, r);
             }
-            tc::wait_st();
           }
+          bool zeroed = false;
           if (s == 0 && j == it.n_kv - 1 && kpos0 + BN > it.kv_len) {
             // Rows past kv_len may hold stale/uninitialised bytes of the last
             // mapped chunk: zero them so 0 * NaN cannot reach the accumulator.
-            // (Every PV of this tile is issued after slot 0's first P half,
-            // which this warpgroup hands over after the fence below.)
-            const int uv = u0 + 2 * j + 1;  // the last block's V
-            const int st = uv % kRing;
-            mbar_wait(&sm.kv_full[st], (uv / kRing) & 1);
+            // (Slot 1's PV of this tile is issued after slot 0's P arrives.)
+            const int st = g % kStages;
+            mbar_wait(&sm.v_full[st], (g / kStages) & 1);
             if (kpos0 + row >= it.kv_len) {
               const uint4 z = make_uint4(0, 0, 0, 0);
-              uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.kv[st][0]) + row * 128);
-              uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.kv[st][1]) + row * 128);
+              uint4* r0 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][0]) + row * 128);
+              uint4* r1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.v[st][1]) + row * 128);
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
                 r0[c] = z;
                 r1[c] = z;
               }
             }
+            zeroed = true;
           }
           float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                            make_float2(0.f, 0.f)};
-          // Two halves of 64 keys: P of keys 0-63 is stored and handed to the
-          // MMA warp (its PV half runs) while the second half is exponentiated.
+          // Two halves of 64 keys: P of keys 0-63 goes to TMEM columns 0-31 and
+          // is handed to the MMA warp (its PV half runs) while the second half
+          // is exponentiated. Column c = keys (2c, 2c+1) as bf16x2.
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
             uint32_t pr[BN / 4];
@@ -533,17 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               acc[k & 3] = __fadd2_rn(acc[k & 3], e);
               pr[k2] = pack_bf16(e.x, e.y);
             }
-            // P(j-1) must have been read by its PV before it is overwritten.
-            if (hf == 0 && g >= 1) mbar_wait(&sm.o_done[s], (g - 1) & 1);
-            const uint32_t dst = p_row + static_cast<uint32_t>(hf * BM * 128);
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                               dst + static_cast<uint32_t>((c ^ (row & 7)) << 4)),
-                           "r"(pr[4 * c]), "r"(pr[4 * c + 1]), "r"(pr[4 * c + 2]), "r"(pr[4 * c + 3])
-                           : "memory");
-            fence_proxy_async_smem();  // generic-proxy stores -> the tensor core's reads
-            if (hf == 0) tc::fence_before();  // orders the O rescale's tcgen05.st too
+            tmem_st32(s_addr + 32 * hf, pr);
+            tc::wait_st();
+            if (hf == 0 && zeroed) fence_proxy_async_smem();
+            tc::fence_before();
             mbar_arrive(&sm.p_full[s][hf]);
           }
           const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
@@ -552,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           VT_SUB(row == 0 && s == 0, g, 3);
           VT_TRACE(row == 0, g, 2 * s + 1);
         }
-        // epilogue: wait for the item's last PV.
+        // epilogue: PV(n_kv-2) completed before S(n_kv-1); wait for the last PV.
         VT_TRACE(row == 0 && s == 0, g - 1, 6);
         mbar_wait(&sm.o_done[s], (g - 1) & 1);
         tc::fence_after();
@@ -573,13 +531,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < D; k += 16) {
             uint32_t w8[8];
 #pragma unroll
-            for (int u8 = 0; u8 < 8; ++u8)
-              w8[u8] = pack_bf16(__uint_as_float(r[k + 2 * u8]) * inv, __uint_as_float(r[k + 2 * u8 + 1]) * inv);
+            for (int u = 0; u < 8; ++u)
+              w8[u] = pack_bf16(__uint_as_float(r[k + 2 * u]) * inv, __uint_as_float(r[k + 2 * u + 1]) * inv);
             asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + k),
                          "r"(w8[0]), "r"(w8[1]), "r"(w8[2]), "r"(w8[3]), "r"(w8[4]), "r"(w8[5]),
                          "r"(w8[6]), "r"(w8[7])
                          : "memory");
           }
+
         }
         // O is read: the next item's PV(0) (acc = 0) may overwrite it. That
         // PV waits for this warpgroup's next P, which comes after this point.

@@ -60,6 +60,9 @@ struct Driver {
   CUresult (*PrimaryCtxRelease)(CUdevice);
   CUresult (*CtxSetCurrent)(CUcontext);
   CUresult (*CtxGetCurrent)(CUcontext*);
+  CUresult (*CtxCreate)(CUcontext*, unsigned int, CUdevice);
+  CUresult (*CtxDestroy)(CUcontext);
+  CUresult (*CtxPopCurrent)(CUcontext*);
   CUresult (*AddrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
   CUresult (*AddrFree)(CUdeviceptr, size_t);
   CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
@@ -116,6 +119,9 @@ Driver& driver() {
     VT_SYM(PrimaryCtxRelease, "cuDevicePrimaryCtxRelease_v2");
     VT_SYM(CtxSetCurrent, "cuCtxSetCurrent");
     VT_SYM(CtxGetCurrent, "cuCtxGetCurrent");
+    VT_SYM(CtxCreate, "cuCtxCreate_v2");
+    VT_SYM(CtxDestroy, "cuCtxDestroy_v2");
+    VT_SYM(CtxPopCurrent, "cuCtxPopCurrent_v2");
     VT_SYM(AddrReserve, "cuMemAddressReserve");
     VT_SYM(AddrFree, "cuMemAddressFree");
     VT_SYM(MemCreate, "cuMemCreate");
@@ -201,6 +207,12 @@ struct vt_device {
 
   // --- CUDA backend ---
   CUcontext ctx = nullptr;
+  // Context the driver worker (and pool) issue the VMM calls from: the
+  // primary context, or with VT_WORKER_CTX=1 a private one on the same
+  // device (mappings are per device, so kernels in the primary context see
+  // them; tools/vmm_probe5.cu measured the calls there under chained launches).
+  CUcontext work_ctx = nullptr;
+  bool own_work_ctx = false;
   CUdevice cu_dev = 0;
   CUmemAllocationProp prop{};
   CUmemAccessDesc access{};
@@ -437,7 +449,7 @@ struct vt_device {
     }
   }
   void pool_main() {
-    driver().CtxSetCurrent(ctx);
+    driver().CtxSetCurrent(work_ctx);
     uint64_t seen = 0;
     for (;;) {
       const std::function<void(size_t)>* fn;
@@ -682,7 +694,7 @@ struct vt_device {
   }
 
   void worker_main() {
-    driver().CtxSetCurrent(ctx);
+    driver().CtxSetCurrent(work_ctx);
     std::vector<DrvOp> batch;
     for (;;) {
       {
@@ -846,6 +858,17 @@ int vt_dev_open(const vt_config* cfg, int cuda_ordinal, vt_device** out) {
     if (const char* e = std::getenv("VT_DRIVER_THREADS")) threads = std::atoi(e);
     d->driver_threads = std::max(1, std::min(threads, 16));
     if (const char* e = std::getenv("VT_SETACCESS_RUNS")) d->setaccess_runs = std::atoi(e) != 0;
+    d->work_ctx = d->ctx;
+    if (const char* e = std::getenv("VT_WORKER_CTX")) {
+      if (std::atoi(e) != 0) {
+        CUcontext c = nullptr, popped = nullptr;
+        if (drv.CtxCreate(&c, 0, dev) == CUDA_SUCCESS) {
+          drv.CtxPopCurrent(&popped);  // cuCtxCreate pushed it on this thread
+          d->work_ctx = c;
+          d->own_work_ctx = true;
+        }
+      }
+    }
     d->start_pool(d->driver_threads);
     d->worker = std::thread([d] { d->worker_main(); });
   }
@@ -881,6 +904,7 @@ int vt_dev_close(vt_device* d) {
       if (ev) drv.EventDestroy(ev);
     if (d->fence_src) drv.EventDestroy(d->fence_src);
     if (d->fence_stream) drv.StreamDestroy(d->fence_stream);
+    if (d->own_work_ctx) drv.CtxDestroy(d->work_ctx);
     drv.PrimaryCtxRelease(d->cu_dev);
   }
   delete d;
