@@ -48,8 +48,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "../../include/vt_attention.h"
-#include "vt_tc_common.cuh"
+#include "vt_pf_common.cuh"
 
 namespace vt {
 namespace pf {
@@ -83,61 +85,6 @@ struct __align__(1024) Smem {
   uint64_t o_done[kSlots];
   uint32_t tmem_base;
 };
-
-#define VT_R32(x)                                                                              \
-  "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),          \
-      "=r"(x[7]), "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]),  \
-      "=r"(x[14]), "=r"(x[15]), "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]),            \
-      "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]), "=r"(x[24]), "=r"(x[25]),            \
-      "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
-#define VT_W32(x)                                                                              \
-  "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]),      \
-      "r"(x[8]), "r"(x[9]), "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(x[13]), "r"(x[14]),        \
-      "r"(x[15]), "r"(x[16]), "r"(x[17]), "r"(x[18]), "r"(x[19]), "r"(x[20]), "r"(x[21]),      \
-      "r"(x[22]), "r"(x[23]), "r"(x[24]), "r"(x[25]), "r"(x[26]), "r"(x[27]), "r"(x[28]),      \
-      "r"(x[29]), "r"(x[30]), "r"(x[31])
-
-// 32 consecutive 32-bit TMEM columns of this thread's lane (no wait).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : VT_R32(r)
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-          taddr),
-      VT_W32(r)
-      : "memory");
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// 2^x for a pair on the FMA pipe (offloads MUFU): round-to-nearest split
-// x = n + f, f in [-1/2, 1/2], cubic fit of 2^f (max relative error 1.1e-4,
-// far below the 3.9e-3 of the bf16 P it feeds), exponent added as integer
-// bits. Clamped at -125 (2^-125 ~ 2e-38 stands in for exp(-inf) = 0: P of a
-// masked key is that small, and masked V rows are finite or zeroed); x <= 127.
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -125.0f);
-  x.y = fmaxf(x.y, -125.0f);
-  const float2 big = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
-  const float2 t = __fadd2_rn(x, big);                       // n in the low mantissa bits
-  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
-  float2 p = __ffma2_rn(make_float2(0.054598168f, 0.054598168f), f,
-                        make_float2(0.24221788f, 0.24221788f));
-  p = __ffma2_rn(p, f, make_float2(0.69336749f, 0.69336749f));
-  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
-  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
 
 #ifdef VT_PF_TRACE
 // Debug timeline of CTA 0 (clock64), per global key block g < 256:
@@ -565,11 +512,24 @@ extern "C" int vt_prefill_trace(long long* out) {  // 256 x 8 + 256 x 4 values
 }
 #endif
 
+namespace vt {
+int launch_prefill_pair(const vt_kv_geometry* g, int32_t layer, const void* q, const void* kv_maps,
+                        const int32_t* start, const int32_t* q_off, int32_t batch,
+                        int32_t max_n_new, int64_t total, float scale, void* out, void* stream);
+}
+
 namespace {
 
 int launch_prefill(const vt_kv_geometry* g, int32_t layer, const void* q, const void* kv_maps,
                    const int32_t* start, const int32_t* q_off, int32_t batch, int32_t max_n_new,
                    int64_t total, float scale, void* out, void* stream) {
+  static const bool pair = [] {
+    const char* e = std::getenv("VT_PREFILL_PAIR");
+    return e && std::atoi(e) != 0;
+  }();
+  if (pair)
+    return vt::launch_prefill_pair(g, layer, q, kv_maps, start, q_off, batch, max_n_new, total,
+                                   scale, out, stream);
   if (g->head_dim != D || g->q_heads % g->kv_heads) return cudaErrorInvalidValue;
   if (batch <= 0 || max_n_new <= 0 || total <= 0) return 0;
   // Q as one packed [total tokens][Hq][D] tensor (a 4-D map with a unit outer
