@@ -626,6 +626,8 @@ def run_ours(args, world, rank, local):
     bounds0 = wl.boundaries
     drv0 = wl.dev.driver_stats()
     wl.dev.driver_latencies("map_page", reset=True)
+    wl.dev.driver_latencies("cuMemMap", reset=True)
+    wl.dev.driver_latencies("cuMemSetAccess", reset=True)
     wl.extend_ns.clear()
     mapped0 = wl.chunks_mapped
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -725,6 +727,13 @@ def run_ours(args, world, rank, local):
                "pipeline": "copies on a side stream overlap the previous/next step (double-buffered)"}
 
     map_lat = sorted(wl.dev.driver_latencies("map_page")) or [0]
+
+    def call_stats(name):  # raw driver call durations inside the timed region
+        v = sorted(wl.dev.driver_latencies(name)) or [0]
+        return {"calls": len(v) if v != [0] else 0, "us_p50": round(v[len(v) // 2] / 1e3, 1),
+                "us_p99": round(v[min(len(v) - 1, int(len(v) * 0.99))] / 1e3, 1),
+                "us_max": round(v[-1] / 1e3, 1)}
+    raw_calls = {"cuMemMap": call_stats("cuMemMap"), "cuMemSetAccess": call_stats("cuMemSetAccess")}
     drv_end = wl.dev.driver_stats()
     drv = {k: drv_end[k] - drv0[k] for k in drv_end}  # timed region only
     peaks = {}
@@ -803,6 +812,7 @@ def run_ours(args, world, rank, local):
                 "driver_map_us_mean": round(drv["map_ns_total"] / max(drv["map_calls"], 1) / 1e3, 2),
                 "driver_create_us_mean": round(drv["create_ns_total"] / max(drv["create_calls"], 1) / 1e3, 2),
                 "driver_access_us_mean": round(drv["access_ns_total"] / max(drv["access_calls"], 1) / 1e3, 2),
+                "driver_calls": raw_calls,
                 "gpu_stalled_steps": stalls,
                 "gpu_idle_between_steps_ms": round(sum(gaps), 3),
                 "gpu_idle_gap_ms_max": round(max(gaps), 3) if gaps else 0.0,

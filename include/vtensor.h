@@ -196,7 +196,8 @@ int vt_set_phys_reserve(vt_device* dev, int64_t chunks);
 /* Submit -> completed latency (ns) of every driver op of kind `op` (a vt_op
  * code: create/map/unmap/destroy/release) completed since the last reset;
  * copies up to `cap` samples, *n = total available. reset != 0 clears. This
- * is the "vTensor extend latency" distribution (p50/p99) for maps. */
+ * is the "vTensor extend latency" distribution (p50/p99) for maps. op 6 / 7:
+ * the duration of each raw cuMemMap / cuMemSetAccess call the worker made. */
 int vt_driver_latencies(vt_device* dev, int32_t op, int64_t* ns_out, int64_t cap, int64_t* n,
                         int reset);
 

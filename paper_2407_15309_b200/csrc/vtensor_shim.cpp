@@ -253,7 +253,9 @@ struct vt_device {
   int driver_threads = 1;
   bool setaccess_runs = false;  // one cuMemSetAccess per contiguous run of maps (VT_SETACCESS_RUNS=1)
   std::mutex lat_mu;
-  std::vector<int64_t> lat[6];  // per vt_op: submit -> completed, ns
+  // [0,6): per vt_op, submit -> completed (ns); 6 / 7: duration of each raw
+  // cuMemMap / cuMemSetAccess driver call (ns)
+  std::vector<int64_t> lat[8];
 
   bool is_cuda() const { return ordinal >= 0; }
 
@@ -265,6 +267,11 @@ struct vt_device {
     std::lock_guard<std::mutex> lk(lat_mu);
     auto& v = lat[kOp[static_cast<int>(op.kind)]];
     if (v.size() < (1u << 20)) v.push_back(done_ns - op.submit_ns);
+  }
+  void note_call(int ring, int64_t ns) {
+    std::lock_guard<std::mutex> lk(lat_mu);
+    auto& v = lat[ring];
+    if (v.size() < (1u << 20)) v.push_back(ns);
   }
   // Imported chunks live in another device's pool and budget.
   int64_t created_bytes() const {
@@ -518,6 +525,8 @@ struct vt_device {
     r = d.MemSetAccess(op.addr, len, &access, 1);
     if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
     int64_t t1 = now_ns();
+    note_call(6, ta - t0);
+    note_call(7, t1 - ta);
     std::lock_guard<std::mutex> lk(stat_mu);
     dstats.map_calls++;
     dstats.access_calls++;
@@ -539,7 +548,9 @@ struct vt_device {
                      std::to_string(ops[mapped].handle_id) + ")");
         break;
       }
+      const int64_t tm = now_ns();
       CUresult r = d.MemMap(ops[mapped].addr, len, 0, h, 0);
+      note_call(6, now_ns() - tm);
       if (r != CUDA_SUCCESS) {
         record_error("cuMemMap: " + cu_err(r));
         break;
@@ -551,6 +562,7 @@ struct vt_device {
       if (r != CUDA_SUCCESS) record_error("cuMemSetAccess: " + cu_err(r));
     }
     int64_t t1 = now_ns();
+    if (mapped) note_call(7, t1 - ta);
     std::lock_guard<std::mutex> lk(stat_mu);
     dstats.map_calls += static_cast<int64_t>(mapped);
     dstats.access_calls++;
@@ -1362,7 +1374,7 @@ int vt_set_phys_reserve(vt_device* d, int64_t chunks) {
 
 int vt_driver_latencies(vt_device* d, int32_t op, int64_t* ns_out, int64_t cap, int64_t* n,
                         int reset) {
-  if (op < 0 || op > 5) return VT_E_ARG;
+  if (op < 0 || op > 7) return VT_E_ARG;
   std::lock_guard<std::mutex> lk(d->lat_mu);
   auto& v = d->lat[op];
   *n = static_cast<int64_t>(v.size());

@@ -518,8 +518,11 @@ class VirtualMemoryDevice:
             self._raise(rc)
 
     def driver_latencies(self, op: str = "map_page", reset: bool = False) -> list[int]:
-        """Submit->completed latency (ns) of the driver ops of one kind."""
-        code = N.OP_NAMES.index(op)
+        """Submit->completed latency (ns) of the driver ops of one kind, or
+        (op "cuMemMap" / "cuMemSetAccess") the duration of each raw call."""
+        code = {"cuMemMap": 6, "cuMemSetAccess": 7}.get(op)
+        if code is None:
+            code = N.OP_NAMES.index(op)
         n = ctypes.c_int64()
         self._lib.vt_driver_latencies(self._h, code, None, 0, ctypes.byref(n), 0)
         buf = (ctypes.c_int64 * max(n.value, 1))()
