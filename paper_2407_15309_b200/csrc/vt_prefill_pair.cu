@@ -106,9 +106,13 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
   return r;
 }
+// Arrive on the leader's barrier. Default (.release.cta) semantics: the data
+// handed over lives in TMEM / is read by the tensor core, ordered by
+// tcgen05.wait + tcgen05.fence::before_thread_sync ahead of this arrive; a
+// .release.cluster arrive compiles to MEMBAR.ALL.GPU and was 23% of the
+// kernel's stall samples (ncu, profiles/r02).
 __device__ __forceinline__ void arrive_leader(const uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(bar))
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(bar)) : "memory");
 }
 // 2-CTA TMA: lands in this CTA's shared memory, completes bytes on the
 // LEADER's mbarrier.
@@ -161,6 +165,17 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[15])
       : "memory");
 }
+
+#ifdef VT_PF2_TRACE
+// Debug timeline of pair 0 (clock64 of the leader CTA), per global block g <
+// 256: [0]/[2] half A/B S ready at softmax row 0, [1]/[3] P_A/P_B arrived,
+// [4] S_A(g+1), [5] PV_A(g), [6] S_B(g+1), [7] PV_B(g) issued.
+__device__ long long g_pf2_trace[256][8];
+#define PF2_TRACE(cond, g, k) \
+  if ((cond) && blockIdx.x == 0 && (g) < 256) g_pf2_trace[(g)][(k)] = clock64();
+#else
+#define PF2_TRACE(cond, g, k)
+#endif
 
 struct Args {
   __nv_bfloat16* out;       // [total, Hq, D]
@@ -388,18 +403,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // S_A(g+1) once both softmaxes hold S_A(g)
           if (s_more) {
             wait_fence(&sm.s_free[0], g & 1);
+            PF2_TRACE(lane == 0, g, 4);
             issue_s(g + 1, ns, js, 0, js == its.n_blk - 1);
           }
           // PV_A(g)
           if (j == 0 && n >= 1) wait_fence(&sm.o_free, (n - 1) & 1);  // epilogue read O
           wait_fence(&sm.p_full[0], g & 1);
+          PF2_TRACE(lane == 0, g, 5);
           issue_pv(g, j, 0, last_of_item);
           if (s_more) {
             wait_fence(&sm.s_free[1], g & 1);
+            PF2_TRACE(lane == 0, g, 6);
             issue_s(g + 1, ns, js, 1, js == its.n_blk - 1);
             adv_s();
           }
           wait_fence(&sm.p_full[1], g & 1);
+          PF2_TRACE(lane == 0, g, 7);
           issue_pv(g, j, 1, last_of_item);
           if (++j == it.n_blk) {
             w = next_valid(w + n_pairs);
@@ -435,6 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int hf = 0; hf < 2; ++hf) {
           mbar_wait(&sm.s_full[hf], g & 1);
           tc::fence_after();
+          PF2_TRACE(r == 0 && row == 0, g, 2 * hf);
           float x[128];
           {
             uint32_t rr[128];
@@ -491,6 +511,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             tc::wait_st();
           }
+          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+          uint32_t pr[64];
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
+            if ((kPolyMask >> (k & 7)) & 1u) {
+              e = ex2_poly2(e);
+            } else {
+              e.x = tc::ex2(e.x);
+              e.y = tc::ex2(e.y);
+            }
+            acc[k & 3] = __fadd2_rn(acc[k & 3], e);
+            pr[k] = pack_bf16(e.x, e.y);
+          }
           if (hf == 0) {
             // This CTA's V half of the block has landed (the leader's PV waits
             // for this warp's P, so p_full implies both halves are in place).
@@ -511,21 +546,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               fence_proxy_async_smem();
             }
           }
-          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                           make_float2(0.f, 0.f)};
-          uint32_t pr[64];
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            float2 e = __ffma2_rn(make_float2(x[2 * k], x[2 * k + 1]), sl2v, negm);
-            if ((kPolyMask >> (k & 7)) & 1u) {
-              e = ex2_poly2(e);
-            } else {
-              e.x = tc::ex2(e.x);
-              e.y = tc::ex2(e.y);
-            }
-            acc[k & 3] = __fadd2_rn(acc[k & 3], e);
-            pr[k] = pack_bf16(e.x, e.y);
-          }
           // P of this half replaces the previous block's: its PV must be done
           if (g >= 1) mbar_wait(&sm.pv_done[hf], (g - 1) & 1);
           // natural key order: tile 2j keys 64hf.. -> P cols 32hf..; tile 2j+1 -> 64 + 32hf
@@ -535,6 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc::fence_before();
           __syncwarp();
           if (lane == 0) arrive_leader(&sm.p_full[hf]);
+          PF2_TRACE(r == 0 && row == 0, g, 2 * hf + 1);
           const float2 a01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
           l_run = fmaf(l_run, alpha, a01.x + a01.y);
           m_run = m_new;
@@ -576,6 +597,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace pf2
+
+#ifdef VT_PF2_TRACE
+extern "C" int vt_prefill_pair_trace(long long* out) {  // 256 x 8 values
+  return cudaMemcpyFromSymbol(out, pf2::g_pf2_trace, sizeof(pf2::g_pf2_trace));
+}
+#endif
 
 // Host launcher (called by vt_prefill.cu's entry points when the pair kernel
 // applies): same arguments as launch_prefill.
