@@ -103,6 +103,9 @@ def parse():
     ap.add_argument("--plain-adaptive", action="store_true",
                     help="apply --plain-every only to steps enqueued while the shim's driver "
                          "worker still has mapping work outstanding")
+    ap.add_argument("--max-ahead", type=int, default=2,
+                    help="steps the host may queue ahead of the GPU before waiting for the "
+                         "oldest (a serving loop reads tokens back every step); 0 = unbounded")
     ap.add_argument("--check", action="store_true",
                     help="after the timed region, compare sampled (request, layer) outputs of the "
                          "last step (and the config-3 prefill probe) with the CPU oracle")
@@ -373,6 +376,8 @@ class DecodeWorkload:
         self.plain_every = 0  # see --plain-every
         self.plain_adaptive = False
         self.boundaries = 0  # plain decode launches (kernel boundaries) enqueued
+        self.max_ahead = 2  # steps the host may have queued ahead of the GPU (0 = unbounded)
+        self.inflight: list = []
         self.last_done = None
         self.gap_events: list | None = None  # (previous step's end, this step's start)
         self.extend_ns: list[int] = []
@@ -460,6 +465,12 @@ class DecodeWorkload:
         k_new = self.k_new if k_new is None else k_new
         v_new = self.v_new if v_new is None else v_new
         out = self.out if out is None else out
+        # Bounded run-ahead: a serving loop reads each step's tokens back, so
+        # the host never queues more than `max_ahead` steps beyond the GPU.
+        # (Unbounded, the host queued ~30 steps of chained launches, and the
+        # driver's cuMemSetAccess tails grew to 100-350 ms: profiles/r02.)
+        while self.max_ahead and len(self.inflight) >= self.max_ahead:
+            self.inflight.pop(0).synchronize()
         # the only pages this step touches: the chunk of each request's new token
         ticket = 0
         for grp in self.groups:
@@ -528,6 +539,7 @@ class DecodeWorkload:
         self.dev.fence(self.stream.cuda_stream)
         self.last_done = torch.cuda.Event(enable_timing=self.gap_events is not None)
         self.last_done.record(self.stream)
+        self.inflight.append(self.last_done)
         for grp in self.groups:
             for rid in self.rids:
                 grp.sched.append_token(rid, 1)
@@ -600,6 +612,7 @@ def run_ours(args, world, rank, local):
                             phys_reserve=0 if args.premap else args.phys_reserve,
                             driver_threads=args.driver_threads, lead_chunks=args.lead_chunks)
     wl.plain_every, wl.plain_adaptive = args.plain_every, args.plain_adaptive
+    wl.max_ahead = args.max_ahead
     wl.dev.wait()  # the physical reserve (if any) is filled before any timing
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -820,6 +833,7 @@ def run_ours(args, world, rank, local):
                 "chained_steps": chained,
                 "plain_decode_launches_per_step": round(plain_per_step, 2),
                 "plain_every": args.plain_every,
+                "max_steps_ahead": args.max_ahead,
                 "plain_adaptive": args.plain_adaptive,
                 "lead_chunks": wl.lead_chunks,
                 "ready_note": ("chained layers leave the driver one plain kernel boundary per "
