@@ -178,10 +178,12 @@ def dist_setup(args):
     max/sum of the timings. When more ranks than GPUs are launched (checking
     the N-rank mechanics on a 1-GPU box) ranks share devices round-robin, the
     timing reductions go over gloo (NCCL refuses two ranks on one GPU);
-    numbers from such a run are not scaling numbers, and two processes'
-    tcgen05 kernels time-sliced on one GPU occasionally stall (seen in ~1 of 3
-    two-rank runs) — a mechanics check only, never the driver's
-    one-rank-per-GPU configuration."""
+    numbers from such a run are not scaling numbers — a mechanics check only,
+    never the driver's one-rank-per-GPU configuration. Two processes' tcgen05
+    /TMEM kernels time-sliced on one GPU stall (r02 bisect: tcgen05 decode
+    hung 4 of 4 two-rank runs, chained or not; the CUDA-core decode, which
+    holds no TMEM, completed 2 of 2), so an oversubscribed run uses the
+    CUDA-core path and says so in its config."""
     global _COLL_DEVICE
     import torch
 
@@ -199,6 +201,11 @@ def dist_setup(args):
         else:
             dist.init_process_group("gloo")
             _COLL_DEVICE = "cpu"
+            if args.path == "tcgen05":
+                args.path = "cuda_core"
+                args.oversubscribed = ("%d ranks share %d GPU(s): decode on the CUDA-core path "
+                                       "(time-sliced tcgen05/TMEM kernels of two processes stall)"
+                                       % (world, n_dev))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, torch.cuda.current_device() if torch.cuda.is_available() else local
@@ -791,7 +798,9 @@ def run_ours(args, world, rank, local):
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (seeded randn bf16 KV in real cuMemMap'd 2 MiB chunks)",
-            "config": workload_config(args.config, world, args.split, args.path, args.growth),
+            "config": dict(workload_config(args.config, world, args.split, args.path, args.growth),
+                           **({"oversubscribed": args.oversubscribed}
+                              if getattr(args, "oversubscribed", None) else {})),
             "tokens_per_s": round(tokens_all / (elapsed_max * 1e-3), 1),
             "hbm_frac_of_step": round(value / hbm_peak, 4),
             "roofline": {
