@@ -106,6 +106,9 @@ def parse():
     ap.add_argument("--max-ahead", type=int, default=2,
                     help="steps the host may queue ahead of the GPU before waiting for the "
                          "oldest (a serving loop reads tokens back every step); 0 = unbounded")
+    ap.add_argument("--host-sync", choices=["spin", "poll", "block"], default="spin",
+                    help="how the host waits for its oldest queued step: spin in the driver "
+                         "(default), poll with short sleeps, or a blocking-sync event")
     ap.add_argument("--check", action="store_true",
                     help="after the timed region, compare sampled (request, layer) outputs of the "
                          "last step (and the config-3 prefill probe) with the CPU oracle")
@@ -384,6 +387,7 @@ class DecodeWorkload:
         self.plain_adaptive = False
         self.boundaries = 0  # plain decode launches (kernel boundaries) enqueued
         self.max_ahead = 2  # steps the host may have queued ahead of the GPU (0 = unbounded)
+        self.host_sync = "spin"  # how the host waits for the oldest queued step (--host-sync)
         self.inflight: list = []
         self.last_done = None
         self.gap_events: list | None = None  # (previous step's end, this step's start)
@@ -477,7 +481,12 @@ class DecodeWorkload:
         # (Unbounded, the host queued ~30 steps of chained launches, and the
         # driver's cuMemSetAccess tails grew to 100-350 ms: profiles/r02.)
         while self.max_ahead and len(self.inflight) >= self.max_ahead:
-            self.inflight.pop(0).synchronize()
+            ev = self.inflight.pop(0)
+            if self.host_sync == "poll":  # short driver calls: never block inside the driver
+                while not ev.query():
+                    time.sleep(2e-5)
+            else:
+                ev.synchronize()
         # the only pages this step touches: the chunk of each request's new token
         ticket = 0
         for grp in self.groups:
@@ -544,7 +553,8 @@ class DecodeWorkload:
                 run_events[gi][1].record(self.stream)
         self.seq, self.seq1 = self.seq1, self.seq
         self.dev.fence(self.stream.cuda_stream)
-        self.last_done = torch.cuda.Event(enable_timing=self.gap_events is not None)
+        self.last_done = torch.cuda.Event(enable_timing=self.gap_events is not None,
+                                          blocking=self.host_sync == "block")
         self.last_done.record(self.stream)
         self.inflight.append(self.last_done)
         for grp in self.groups:
@@ -620,6 +630,7 @@ def run_ours(args, world, rank, local):
                             driver_threads=args.driver_threads, lead_chunks=args.lead_chunks)
     wl.plain_every, wl.plain_adaptive = args.plain_every, args.plain_adaptive
     wl.max_ahead = args.max_ahead
+    wl.host_sync = args.host_sync
     wl.dev.wait()  # the physical reserve (if any) is filled before any timing
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -843,6 +854,7 @@ def run_ours(args, world, rank, local):
                 "plain_decode_launches_per_step": round(plain_per_step, 2),
                 "plain_every": args.plain_every,
                 "max_steps_ahead": args.max_ahead,
+                "host_sync": args.host_sync,
                 "plain_adaptive": args.plain_adaptive,
                 "lead_chunks": wl.lead_chunks,
                 "ready_note": ("chained layers leave the driver one plain kernel boundary per "
