@@ -106,6 +106,9 @@ def parse():
     ap.add_argument("--max-ahead", type=int, default=2,
                     help="steps the host may queue ahead of the GPU before waiting for the "
                          "oldest (a serving loop reads tokens back every step); 0 = unbounded")
+    ap.add_argument("--clock-interval", type=float, default=0.05,
+                    help="seconds between NVML clock samples in the timed region (each NVML "
+                         "query enters the kernel driver, like the VMM calls)")
     ap.add_argument("--host-sync", choices=["spin", "poll", "block"], default="spin",
                     help="how the host waits for its oldest queued step: spin in the driver "
                          "(default), poll with short sleeps, or a blocking-sync event")
@@ -125,8 +128,9 @@ class ClockSampler:
         "hw_thermal_slowdown": 0x40,
     }
 
-    def __init__(self, index: int) -> None:
+    def __init__(self, index: int, interval: float = 0.05) -> None:
         self.index = index
+        self.interval = interval
         self.samples: list[tuple[int, int, int]] = []
         self._stop = threading.Event()
         self._t = None
@@ -146,7 +150,7 @@ class ClockSampler:
                 except AttributeError:  # older bindings
                     reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.samples.append((sm, mx, reasons))
-                self._stop.wait(0.05)
+                self._stop.wait(self.interval)
         except Exception as exc:  # pragma: no cover - no NVML
             self._nvml = repr(exc)
 
@@ -662,7 +666,7 @@ def run_ours(args, world, rank, local):
     wl.extend_ns.clear()
     mapped0 = wl.chunks_mapped
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local, args.clock_interval) as clocks:
         torch.cuda.synchronize()
         barrier(world)
         start.record()
@@ -882,7 +886,7 @@ def run_ours(args, world, rank, local):
             "prefill_cfg3": prefill,
             "qkv_append": qkv,
             "premapped": bool(args.premap),
-            "clocks": clocks.summary(),
+            "clocks": dict(clocks.summary(), interval_s=args.clock_interval),
         }
         print(json.dumps(line))
     wl.dev.wait()

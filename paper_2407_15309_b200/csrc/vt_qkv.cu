@@ -70,6 +70,12 @@ struct Cfg {
   static constexpr int kStageBytes = kBlockBytes + kXBytes;
   static constexpr int kStages = kRingBytes / kStageBytes;
   static constexpr int kTmemCols = NT;
+  // K-split pair: the peer's fp32 partial of this CTA's token half lands in a
+  // buffer of its own (when it fits beside the ring), so it can be sent the
+  // moment the peer's accumulator is ready, with no "ring free" handshake
+  static constexpr int kPartialBytes = NT / 2 * 128 * 4;
+  static constexpr bool kDedicated = kPartialBytes <= 16 * 1024;
+  static constexpr size_t kDynSmem = kRingBytes + (kDedicated ? kPartialBytes : 0) + 1024;
   static_assert(kStages >= 2, "ring too small");
   static_assert(NT / 2 * BM * 4 <= kRingBytes, "the peer's half partial must fit the ring");
 };
@@ -153,8 +159,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&acc_full, 1);
     mbar_init(&peer_ready, 1);
-    mbar_init(&partial_full, 1);  // the lower CTA's expect_tx; the bulk copy completes it
+    mbar_init(&partial_full, 1);  // armed with the partial's bytes; the peer's st.async completes it
     fence_mbar_init();
+    // The weights do not depend on the previous kernel or on the peer: the
+    // first ring's worth is issued before the cluster barrier, TMEM
+    // allocation and PDL wait (only this CTA's own barriers are involved).
+    const uint64_t once = l2_evict_first_policy();
+    const int n = kb1 - kb0;
+    const uint64_t wsrc = reinterpret_cast<uint64_t>(a.w_packed) +
+                          (static_cast<uint64_t>(m) * KB + kb0) * kBlockBytes;
+    for (int i = 0; i < min(n, C::kStages); ++i) {
+      mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+      bulk_g2s(ring + i * C::kStageBytes, wsrc + static_cast<uint64_t>(i) * kBlockBytes,
+               kBlockBytes, &full[i], once);
+      if (i == 0) QKV_TRACE(2);
+    }
   }
   if (warp == 1) tc::alloc(&tmem_base, C::kTmemCols);
   tc::fence_before();
@@ -167,6 +186,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_base;
   tc::grid_launch_dependents();  // the next launch may start its own prologue
   if (threadIdx.x == 0) QKV_TRACE(1);
+  if constexpr (KS == 2 && C::kDedicated) {
+    // the peer's partial may land any time after its MMAs: armed up front
+    if (threadIdx.x == 64) mbar_arrive_expect_tx(&partial_full, C::kPartialBytes);
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -179,13 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // previous kernel, so the first ring's worth streams in while that
       // kernel drains; x (its output in a real layer stack) only after
       // griddepcontrol.wait.
-      const int pre = min(n, C::kStages);
-      for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], C::kStageBytes);
-        bulk_g2s(ring + i * C::kStageBytes, wsrc + static_cast<uint64_t>(i) * kBlockBytes,
-                 kBlockBytes, &full[i], once);
-        if (i == 0) QKV_TRACE(2);
-      }
+      const int pre = min(n, C::kStages);  // issued at barrier init
       tc::grid_dependency_wait();
       for (int i = 0; i < n; ++i) {
         const int st = i % C::kStages;
@@ -240,7 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kHalfNT = KS == 2 ? NT / 2 : NT;
     const int my_c0 = static_cast<int>(half) * kHalfNT;          // token columns finalised here
     const int peer_c0 = KS == 2 ? (1 - static_cast<int>(half)) * kHalfNT : 0;
-    float* peer_part = reinterpret_cast<float*>(ring);  // [kHalfNT][BM] fp32 partial from the peer
+    // [kHalfNT][BM] fp32 partial from the peer: its own buffer, or our ring once idle
+    float* peer_part = reinterpret_cast<float*>(C::kDedicated ? ring + kRingBytes : ring);
     {
       const int kind = m < a.hq ? 0 : (m < a.hq + a.hkv ? 1 : 2);  // q | K | V
       const int head = kind == 0 ? m : (kind == 1 ? m - a.hq : m - a.hq - a.hkv);
@@ -272,11 +290,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // our MMAs are done, so our ring is free for the peer's partial; once
       // the peer's is free too, asynchronous remote stores of the peer's half
       // straight from the accumulator, completing bytes on its barrier
-      if (ep == 0) {
-        mbar_arrive_expect_tx(&partial_full, kHalfNT * BM * 4);
-        arrive_peer(peer_addr(&peer_ready, 1 - half));
+      if constexpr (!C::kDedicated) {
+        if (ep == 0) {
+          mbar_arrive_expect_tx(&partial_full, kHalfNT * BM * 4);
+          arrive_peer(peer_addr(&peer_ready, 1 - half));
+        }
+        mbar_wait(&peer_ready, 0);
       }
-      mbar_wait(&peer_ready, 0);
       if (ep == 0) QKV_TRACE(7);
       const uint32_t dst = peer_addr(peer_part, 1 - half);
       const uint32_t bar = peer_addr(&partial_full, 1 - half);
@@ -362,7 +382,7 @@ __global__ void pack_weight_kernel(const uint4* __restrict__ w, int hidden, long
 
 template <int NT, int KS>
 int launch(const CUtensorMap& xm, const Args& a, int mtiles, int ttiles, cudaStream_t stream) {
-  const size_t smem = kRingBytes + 1024;
+  const size_t smem = KS == 2 ? Cfg<NT>::kDynSmem : kRingBytes + 1024;
   static std::atomic<uint64_t> attr_devices{0};
   set_smem_limit_once(qkv_append_kernel<NT, KS>, smem, attr_devices);
   cudaLaunchConfig_t cfg = {};
