@@ -94,8 +94,8 @@ def parse():
     ap.add_argument("--driver-threads", type=int, default=0,
                     help="shim threads executing driver VMM ops in parallel (0 = library default)")
     ap.add_argument("--lead-chunks", type=int, default=0,
-                    help="extend this many chunks ahead of each request's next token (0 = 3 with "
-                         "chained layers, 1 without; the growth trace uses 8)")
+                    help="extend this many chunks ahead of each request's next token (0 = 24: "
+                         "covers the driver's cuMemSetAccess stalls, up to ~1.5 s)")
     ap.add_argument("--plain-every", type=int, default=0,
                     help="with chained decode layers, also launch every N-th layer of a run "
                          "plainly (a kernel boundary where queued cuMemMap/cuMemSetAccess "
@@ -356,12 +356,14 @@ class DecodeWorkload:
         groups = layer_groups(L, hkv)
         tpc = 2 * MIB // groups[0][1].bytes_per_token
         self.map_ahead = int(os.environ.get("VT_MAP_AHEAD", "4"))  # chunks per extend call
-        # extend once headroom drops below this many chunks: a mapping takes
-        # 0.15-2 ms of driver time per chunk (tools/vmm_probe.cu), i.e. a few
-        # steps when several requests cross a chunk edge together
+        # extend once headroom drops below this many chunks. cuMemSetAccess
+        # costs ~0.15-0.8 ms per chunk but stalls for 10-120 ms every ~1 s, in
+        # windows of up to ~1.5 s, even on an idle GPU (tools/vmm_probe7.cu,
+        # profiles/r02/vmm_probes): 24 chunks (384 tokens at 8B, ~2 s of
+        # config-2 decode) rode out every stall in the sustained runs
+        # (profiles/r02/vmm_sustained/r2w_*: 0 host waits; 3 or 12 chunks did not)
         self.chain = chain
-        self.lead_chunks = lead_chunks or int(os.environ.get("VT_LEAD_CHUNKS",
-                                                             "3" if chain else "1"))
+        self.lead_chunks = lead_chunks or int(os.environ.get("VT_LEAD_CHUNKS", "24"))
         win = self.map_ahead * tpc
         self.rids = [f"r{b}" for b in range(B)]
         if start_len:  # growth trace: every request starts at the same length
@@ -518,11 +520,10 @@ class DecodeWorkload:
         mx = max(self.host_lens) + 1
         launches = 1
         # Decode layers after the first are chained (programmatic dependent
-        # launch, vt_decode_attention_chained): +3-4% per step. The driver
-        # completes the worker's concurrent cuMemMap / cuMemSetAccess only at
-        # plain kernel boundaries — one per step when chained — so a mapping
-        # becomes ready several steps after submit; extends are therefore
-        # issued `lead_chunks` chunks ahead (0 host waits, 0 stalls measured).
+        # launch, vt_decode_attention_chained): +3-4% per step. The worker's
+        # concurrent cuMemMap / cuMemSetAccess complete while the chain runs
+        # (probe 6: chained or plain, same per-call cost); their latency tail
+        # is covered by extending `lead_chunks` chunks ahead.
         chain = self.chain
         self.chained_steps += int(chain)
         pe = self.plain_every
@@ -621,9 +622,7 @@ def run_ours(args, world, rank, local):
                             start_len=GROWTH_START, max_seq=32768,
                             phys_reserve=0 if args.premap else args.phys_reserve,
                             driver_threads=args.driver_threads,
-                            # every request crosses a chunk edge every 16 steps for the
-                            # whole trace: cover the driver's tail latency (p99 ~0.2-1 s)
-                            lead_chunks=args.lead_chunks or 8)
+                            lead_chunks=args.lead_chunks)
     else:
         total_steps = args.warmup + 2 * args.steps + 2
         wl = DecodeWorkload(args.config, args.split, seed=1234 + rank, path=args.path,
@@ -861,10 +860,9 @@ def run_ours(args, world, rank, local):
                 "host_sync": args.host_sync,
                 "plain_adaptive": args.plain_adaptive,
                 "lead_chunks": wl.lead_chunks,
-                "ready_note": ("chained layers leave the driver one plain kernel boundary per "
-                               "step, where cuMemMap/cuMemSetAccess complete: ready latency is "
-                               "several steps, covered by extending lead_chunks ahead"
-                               if wl.chain else "plain launches"),
+                "ready_note": ("cuMemSetAccess costs 0.15-0.8 ms per chunk with 10-120 ms "
+                               "stalls (even on an idle GPU, tools/vmm_probe7.cu): ready latency "
+                               "tails are covered by extending lead_chunks ahead"),
                 "host_waited_steps": wl.host_waits - waits0,
                 "hidden": stalls == 0 and wl.host_waits - waits0 == 0,
                 "hidden_rule": ("no step waited on the host for a mapping and the GPU never ran "
@@ -1254,7 +1252,9 @@ def run_reference(args, world, rank):
     v = torch.randn(nb, hkv, ctx, 128, generator=gen).to(torch.bfloat16)
     q = torch.randn(nb, hq, 128, generator=gen).to(torch.bfloat16)
     lens = [ctx] * nb
-    steps, warm = min(args.steps, 10), min(args.warmup, 2)  # bounded: ~0.5 s per step
+    # exactly K timed steps after W warm-up steps; each step is a bounded
+    # sample (one layer of the whole batch: ~0.1-0.2 s on the box's 16 cores)
+    steps, warm = args.steps, args.warmup
     for _ in range(warm):
         decode_attention_torch_cpu(q, k, v, lens)
     t0 = time.perf_counter()
