@@ -409,7 +409,9 @@ class DecodeWorkload:
             self.dev.set_phys_reserve(phys_reserve)
         for grp in self.groups:  # staggered initial headroom (0..win-1 tokens)
             for b, rid in enumerate(self.rids):
-                extra = (premap_steps + win if premap_steps
+                # premap: every token the run appends plus the extend
+                # headroom, so no extend is issued inside the timed region
+                extra = (premap_steps + win + self.lead_chunks * tpc if premap_steps
                          else (self.lead_chunks - 1) * tpc + (b * win) // B)
                 grp.sched.extend(rid, min(self.max_seq, self.lens[b] + 1 + extra))
         self.dev.wait()
