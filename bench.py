@@ -398,6 +398,15 @@ class DecodeWorkload:
         self.last_done = None
         self.gap_events: list | None = None  # (previous step's end, this step's start)
         self.extend_ns: list[int] = []
+        # time-based lead: keep at least `lead_s` seconds of decode mapped
+        # ahead (host step period, EWMA), between lead_chunks and lead_max
+        # chunks — short early steps of the growth trace need more chunks
+        # than config 2's 5 ms steps to cover the same driver stall
+        self.lead_s = 0.0 if premap_steps else float(os.environ.get("VT_LEAD_SECONDS", "2.0"))
+        self.lead_max = int(os.environ.get("VT_LEAD_MAX_CHUNKS", "128"))
+        self.step_s = 0.0
+        self._t_last = None
+        self.lead_eff_max = 0
         self.chunks_mapped = 0
         self._prewarm(1024)
         if phys_reserve < 0:  # auto: the chunks this run will still have to create
@@ -450,12 +459,17 @@ class DecodeWorkload:
         chunks it touches, which were issued steps earlier."""
         for grp in self.groups:
             tpc = grp.tpc
+            lead = self.lead_chunks
+            if self.step_s > 0:
+                lead = min(max(lead, math.ceil(self.lead_s / self.step_s / tpc)),
+                           max(self.lead_max, self.lead_chunks))
+            self.lead_eff_max = max(self.lead_eff_max, lead)
             for b, (rid, length) in enumerate(zip(self.rids, self.host_lens)):
                 space = grp.sched.mem[rid].vt.space
-                if space.mapped_pages * tpc >= length + 1 + self.lead_chunks * tpc:
+                if space.mapped_pages * tpc >= min(self.max_seq, length + 1 + lead * tpc):
                     continue
                 first = space.mapped_pages
-                target = min(self.max_seq, length + 1 + (self.map_ahead + self.lead_chunks - 1) * tpc)
+                target = min(self.max_seq, length + 1 + (self.map_ahead + lead - 1) * tpc)
                 t0 = time.perf_counter_ns()
                 n = grp.sched.extend(rid, target)
                 if n:
@@ -568,6 +582,11 @@ class DecodeWorkload:
             for rid in self.rids:
                 grp.sched.append_token(rid, 1)
         self.host_lens = [n + 1 for n in self.host_lens]
+        now = time.perf_counter()
+        if self._t_last is not None:  # host step period (= GPU step once run-ahead is bounded)
+            dt = now - self._t_last
+            self.step_s = dt if self.step_s == 0 else 0.9 * self.step_s + 0.1 * dt
+        self._t_last = now
         self._issue_extends()  # next steps' pages: overlap with this step's kernels
         return launches
 
@@ -862,6 +881,8 @@ def run_ours(args, world, rank, local):
                 "host_sync": args.host_sync,
                 "plain_adaptive": args.plain_adaptive,
                 "lead_chunks": wl.lead_chunks,
+                "lead_seconds": wl.lead_s,
+                "lead_chunks_max_used": wl.lead_eff_max,
                 "ready_note": ("cuMemSetAccess costs 0.15-0.8 ms per chunk with 10-120 ms "
                                "stalls (even on an idle GPU, tools/vmm_probe7.cu): ready latency "
                                "tails are covered by extending lead_chunks ahead"),
