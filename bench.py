@@ -1123,7 +1123,7 @@ def qkv_probe(layers: int = 32) -> dict:
             "unfused_us_per_layer": round(t_u * 1e6, 2),
             "speedup_vs_unfused": round(t_u / t_f, 3),
             "unfused": "cuBLAS GEMM (torch) + vt_kv_append",
-            "kernel": "vt::qkv::qkv_append_kernel<64,2> (tcgen05, packed weight, K halves on a 2-CTA cluster, DSMEM reduction)",
+            "kernel": "vt::qkv::qkv_append_kernel<64,3> (tcgen05, packed weight; per feature tile a 2-CTA cluster (K halves, DSMEM reduction) + a helper CTA (first K quarter, partial through L2); 144 CTAs)",
             "weight_layout": "packed once (vt_qkv_pack_weight) outside the timed region"}
 
 

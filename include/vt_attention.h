@@ -121,9 +121,7 @@ int vt_prefill_attention_varlen(const vt_kv_geometry* g, int32_t layer, const vo
                                 const int32_t* q_offsets, int32_t batch, int32_t max_n_new,
                                 int64_t total_tokens, float scale, void* out, void* stream);
 
-/* Fused QKV projection + KV append, tcgen05; each
- * 128-feature tile's K halves run on a 2-CTA cluster and are reduced through
- * distributed shared memory (no global workspace):
+/* Fused QKV projection + KV append, tcgen05:
  *   qkv = x . W^T    x [n_tokens, hidden] bf16, W [(Hq+2Hkv)*head_dim, hidden]
  *                    bf16 (nn.Linear layout) passed PACKED (vt_qkv_pack_weight),
  *                    fp32 accumulate
@@ -131,9 +129,26 @@ int vt_prefill_attention_varlen(const vt_kv_geometry* g, int32_t layer, const vo
  * straight into request tok_req[t]'s VA (kv_va[tok_req[t]]) at token position
  * tok_pos[t] of `layer`, in the vt_kv_append layout (the page must be mapped:
  * the manager's extend ticket was waited on, kvsim/scheduler.py:189-205).
- * hidden % 64 == 0. split_k: CTAs per feature tile, 1 or 2 (0 = auto: 2
- * unless the tile grid alone fills the SMs twice over); > 2 is an error.
- *   tok_req, tok_pos : [n_tokens] i32 (device);  kv_va : [n_req] u64 (device) */
+ * hidden % 64 == 0.  tok_req, tok_pos : [n_tokens] i32 (device);
+ * kv_va : [n_req] u64 (device).
+ * split_k = CTAs per 128-feature tile:
+ *   1  one CTA streams the whole hidden dimension;
+ *   2  the K halves on a 2-CTA cluster, reduced through distributed shared
+ *      memory (no workspace);
+ *   3  that pair plus a helper CTA streaming the first quarter of K, its fp32
+ *      partial handed to the pair through L2 (1.5x the SMs streaming);
+ *      n_tokens <= 64 and hidden >= 1024 only, needs `workspace`;
+ *   0  auto: 3 when a workspace is given and the shape allows it, else 2
+ *      unless the tile grid alone fills the SMs twice over, else 1.
+ * workspace: vt_qkv_workspace_bytes(g) bytes, 256-byte aligned, zero-filled
+ * once before first use (its flags reset themselves inside every launch),
+ * private to one stream (launches on that stream may reuse it); NULL allowed
+ * for split_k 0/1/2. vt_qkv_append == vt_qkv_append_ws with workspace NULL. */
+size_t vt_qkv_workspace_bytes(const vt_kv_geometry* g);
+int vt_qkv_append_ws(const vt_kv_geometry* g, int32_t layer, const void* x, const void* w_packed,
+                     int32_t hidden, int32_t n_tokens, const int32_t* tok_req,
+                     const int32_t* tok_pos, const uint64_t* kv_va, void* q_out, int32_t split_k,
+                     void* workspace, void* stream);
 int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x, const void* w_packed,
                   int32_t hidden, int32_t n_tokens, const int32_t* tok_req,
                   const int32_t* tok_pos, const uint64_t* kv_va, void* q_out, int32_t split_k,

@@ -61,6 +61,11 @@ def attn_lib() -> ctypes.CDLL:
         lib.vt_qkv_append.argtypes = [POINTER(_Geo), c_int32, P, P, c_int32, c_int32, P, P, P, P,
                                       c_int32, P]
         lib.vt_qkv_append.restype = c_int
+        lib.vt_qkv_append_ws.argtypes = [POINTER(_Geo), c_int32, P, P, c_int32, c_int32, P, P, P,
+                                         P, c_int32, P, P]
+        lib.vt_qkv_append_ws.restype = c_int
+        lib.vt_qkv_workspace_bytes.argtypes = [POINTER(_Geo)]
+        lib.vt_qkv_workspace_bytes.restype = c_size_t
         lib.vt_qkv_pack_weight.argtypes = [P, c_int32, c_int32, P, P]
         lib.vt_qkv_pack_weight.restype = c_int
         lib.vt_attn_last_launches.argtypes = []
@@ -72,7 +77,7 @@ def attn_lib() -> ctypes.CDLL:
 ATTN_SYMBOLS = ("vt_decode_attention", "vt_decode_attention_chained", "vt_decode_attention_paged",
                 "vt_decode_workspace_bytes", "vt_kv_append",
                 "vt_kv_tensor_maps", "vt_prefill_attention", "vt_prefill_attention_varlen",
-                "vt_qkv_append",
+                "vt_qkv_append", "vt_qkv_append_ws", "vt_qkv_workspace_bytes",
                 "vt_qkv_pack_weight",
                 "vt_attn_last_launches")
 
@@ -206,10 +211,29 @@ def pack_qkv_weight(w_qkv: torch.Tensor,
     return PackedQKVWeight(w_qkv, stream)
 
 
+_QKV_WS: dict = {}
+
+
+def qkv_workspace(geo: KVGeometry, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """The split-3 workspace of ``stream`` (include/vt_attention.h
+    vt_qkv_workspace_bytes): zero-filled once, private to the stream, reused by
+    every launch on it (its flags reset inside each launch)."""
+    s = stream or torch.cuda.current_stream()
+    nbytes = attn_lib().vt_qkv_workspace_bytes(ctypes.byref(_geo(geo)))
+    key = (s.device.index, s.cuda_stream)
+    ws = _QKV_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        with torch.cuda.stream(s):
+            ws = torch.zeros(nbytes, dtype=torch.uint8, device=s.device)
+        _QKV_WS[key] = ws
+    return ws
+
+
 def qkv_append(x: torch.Tensor, w_qkv: "PackedQKVWeight | torch.Tensor", tok_req: torch.Tensor,
                tok_pos: torch.Tensor, kv_va: torch.Tensor, geo: KVGeometry, layer: int,
                q_out: torch.Tensor | None = None, split_k: int = 0,
-               stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+               stream: torch.cuda.Stream | None = None,
+               workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Fused QKV projection + KV append (include/vt_attention.h vt_qkv_append).
 
     x ``[T, hidden]`` bf16; w_qkv a :class:`PackedQKVWeight` of the
@@ -217,9 +241,12 @@ def qkv_append(x: torch.Tensor, w_qkv: "PackedQKVWeight | torch.Tensor", tok_req
     every call — an extra pass over the weight, for one-off use only). Returns
     q ``[T, Hq, d]``; K/V of token t land in the cache of request
     ``tok_req[t]`` at position ``tok_pos[t]`` of ``layer`` (its page must
-    already be mapped). ``split_k`` = CTAs per 128-feature tile: 1, or 2
+    already be mapped). ``split_k`` = CTAs per 128-feature tile: 1, 2
     (the K halves on a 2-CTA cluster, reduced through distributed shared
-    memory); 0 picks automatically."""
+    memory), or 3 (that pair plus a helper CTA whose partial of the first
+    k blocks reaches the pair through L2; T <= 64 only); 0 picks
+    automatically. ``workspace`` defaults to :func:`qkv_workspace` of the
+    stream."""
     T, hidden = x.shape
     feats = (geo.q_heads + 2 * geo.kv_heads) * geo.head_dim
     if isinstance(w_qkv, torch.Tensor):
@@ -231,11 +258,13 @@ def qkv_append(x: torch.Tensor, w_qkv: "PackedQKVWeight | torch.Tensor", tok_req
     if q_out is None:
         q_out = torch.empty(T, geo.q_heads, geo.head_dim, dtype=torch.bfloat16, device=x.device)
     _need_cuda(x, w_qkv.data, tok_req, tok_pos, kv_va, q_out)
-    rc = attn_lib().vt_qkv_append(ctypes.byref(_geo(geo)), layer, x.data_ptr(),
-                                  w_qkv.data.data_ptr(), hidden, T, tok_req.data_ptr(),
-                                  tok_pos.data_ptr(), kv_va.data_ptr(), q_out.data_ptr(), split_k,
-                                  _stream(stream))
-    _check(rc, "vt_qkv_append")
+    if workspace is None:
+        workspace = qkv_workspace(geo, stream)
+    rc = attn_lib().vt_qkv_append_ws(ctypes.byref(_geo(geo)), layer, x.data_ptr(),
+                                     w_qkv.data.data_ptr(), hidden, T, tok_req.data_ptr(),
+                                     tok_pos.data_ptr(), kv_va.data_ptr(), q_out.data_ptr(),
+                                     split_k, workspace.data_ptr(), _stream(stream))
+    _check(rc, "vt_qkv_append_ws")
     return q_out
 
 

@@ -39,6 +39,10 @@
 //   st.async end to end (12.7 us/layer).
 //   Clusters of 2 all co-schedule (74 at one CTA per SM; clusters of 3 do
 //   not: 45 < 48 tiles).
+// * Split 3 (decode default, <= 64 tokens): the pair alone streams on 96 SMs
+//   at ~57 GB/s each, below HBM; a helper CTA per tile takes the first
+//   quarter of K and hands its fp32 partial to the pair through L2 (a
+//   per-stream workspace + a self-resetting flag), so 144 SMs stream.
 //
 // Warp roles (192 threads): warp 0 producer (packed W + x tiles, 192 KiB
 // ring), warp 1 MMA issuer (one elected lane), warps 2-5 epilogue (thread =
@@ -51,6 +55,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
 
 #include "../../include/vt_attention.h"
 #include "vt_tc_common.cuh"
@@ -88,7 +95,21 @@ struct Args {
   const int32_t* tok_pos;     // [T]
   int32_t n_tokens, hq, hkv, tpc, layer, kblocks;
   int64_t chunk_bytes;
+  int32_t mtiles, helper_kb;  // KS == 3: feature tiles, k blocks of each tile's helper CTA
+  float* helper_part;         // KS == 3 workspace: [mtiles][64 tokens][128] fp32
+  int32_t* helper_flag;       //                    [mtiles], zero between launches
 };
+
+// KS == 3 (pair + helper): a third CTA per feature tile streams the first
+// `helper_kb` k blocks and hands its fp32 partial [NT=64 tokens][128 features]
+// to the tile's pair through L2 (each warp store one full 128-byte line); the
+// pair reads it while its own DSMEM hand-off is in flight and adds it last. The helper has
+// fewer blocks than the pair CTAs, so its partial is in L2 before the pair's
+// stream ends. Flags count up (helper +1, each pair CTA +1 after reading) and
+// the last reader resets them, inside one launch (the next launch's helper
+// writes only after griddepcontrol.wait). The partials and flags live in a
+// caller-provided workspace (vt_qkv_workspace_bytes), private to the stream.
+constexpr int kHelperPartFloats = 64 * BM;
 
 // ------------------------------------------------- cluster / DSMEM helpers --
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -114,8 +135,9 @@ __device__ __forceinline__ void arrive_peer(uint32_t bar_addr) {
 // Debug timeline (tools/gpu_trace_qkv.sh): per CTA, %globaltimer at
 // 0 entry, 1 setup done, 2 first W copy issued, 3 first stage landed,
 // 4 last stage landed, 5 last MMA committed, 6 accumulator ready,
-// 7 peer handshake done, 8 partial received / sent, 9 epilogue done.
-__device__ long long g_qkv_trace[512][10];
+// 7 peer handshake done, 8 partial received / sent, 9 epilogue done,
+// 10 (split 3) helper: partial published / pair: helper flag seen.
+__device__ long long g_qkv_trace[512][12];
 __device__ __forceinline__ void trace(int i) {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -137,19 +159,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t full[C::kStages], empty[C::kStages], acc_full;
   __shared__ uint64_t peer_ready;    // the peer CTA's ring is free (its MMAs are done)
   __shared__ uint64_t partial_full;  // the peer's partial of our token half has landed
+  __shared__ uint64_t helper_ready;  // KS == 3: the helper's partial is in L2 (seen by warp 0)
   __shared__ uint64_t row_dst[NT];   // destination of each token's 256-byte head row
   __shared__ __align__(16) __nv_bfloat16 stage_out[4][16][32];  // per epilogue warp
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m = blockIdx.x / KS;                       // feature tile
-  const uint32_t half = KS == 2 ? cluster_rank() : 0;  // K half of this CTA
   const int tt = blockIdx.y;                           // token tile
   const int KB = a.kblocks;
-  const int mid = KS == 2 ? KB / 2 : KB;  // (finishing the lower half earlier was measured: no gain)
-  const int kb0 = half == 0 ? 0 : mid;
-  const int kb1 = half == 0 ? mid : KB;
+  // feature tile, K range, and (KS == 3) whether this CTA is a tile's helper
+  int m, kb0, kb1;
+  uint32_t half = 0;
+  bool helper = false;
+  if constexpr (KS == 3) {
+    const int cl = blockIdx.x >> 1;
+    const uint32_t r = cluster_rank();
+    const int hcl = (a.mtiles + 1) >> 1;  // helper clusters first (dispatched before the pairs)
+    if (cl < hcl) {
+      helper = true;
+      m = cl * 2 + static_cast<int>(r);
+      kb0 = 0;
+      kb1 = m < a.mtiles ? a.helper_kb : 0;  // odd tile count: one idle helper
+    } else {
+      m = cl - hcl;
+      half = r;
+      const int mid = a.helper_kb + (KB - a.helper_kb) / 2;
+      kb0 = r == 0 ? a.helper_kb : mid;
+      kb1 = r == 0 ? mid : KB;
+    }
+  } else {
+    m = blockIdx.x / KS;
+    half = KS == 2 ? cluster_rank() : 0;  // K half of this CTA
+    const int mid = KS == 2 ? KB / 2 : KB;  // (finishing the lower half earlier was measured: no gain)
+    kb0 = half == 0 ? 0 : mid;
+    kb1 = half == 0 ? mid : KB;
+  }
+  const bool pair = KS == 2 || (KS == 3 && !helper);  // exchanges partials with a cluster peer
   if (threadIdx.x == 0) QKV_TRACE(0);
 
   if (threadIdx.x == 0) {
@@ -160,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&acc_full, 1);
     mbar_init(&peer_ready, 1);
     mbar_init(&partial_full, 1);  // armed with the partial's bytes; the peer's st.async completes it
+    mbar_init(&helper_ready, 1);
     fence_mbar_init();
     // The weights do not depend on the previous kernel or on the peer: the
     // first ring's worth is issued before the cluster barrier, TMEM
@@ -177,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tc::alloc(&tmem_base, C::kTmemCols);
   tc::fence_before();
-  if constexpr (KS == 2) {
+  if constexpr (KS >= 2) {
     cluster_sync();  // the peer's barriers are initialised before any remote arrive
   } else {
     __syncthreads();
@@ -186,9 +233,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_base;
   tc::grid_launch_dependents();  // the next launch may start its own prologue
   if (threadIdx.x == 0) QKV_TRACE(1);
-  if constexpr (KS == 2 && C::kDedicated) {
+  if constexpr (KS >= 2 && C::kDedicated) {
     // the peer's partial may land any time after its MMAs: armed up front
-    if (threadIdx.x == 64) mbar_arrive_expect_tx(&partial_full, C::kPartialBytes);
+    if (pair && threadIdx.x == 64) mbar_arrive_expect_tx(&partial_full, C::kPartialBytes);
   }
 
   if (warp == 0) {
@@ -213,6 +260,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_g2s(sw, wsrc + static_cast<uint64_t>(i) * kBlockBytes, kBlockBytes, &full[st], once);
         }
         tc::tma_load_2d(sw + kBlockBytes, &x_map, &full[st], (kb0 + i) * BK, tt * NT, keep);
+      }
+      if constexpr (KS == 3) {
+        // the producer is idle from here: it watches for the helper's partial
+        // (an L2 round trip per poll) so the epilogue does not have to
+        if (!helper) {
+          int f;
+          uint32_t spins = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(a.helper_flag + m) : "memory");
+            if (++spins == (1u << 28)) asm volatile("trap;");  // a lost helper: fail, never hang
+          } while (f < 1);
+          QKV_TRACE(10);
+          mbar_arrive(&helper_ready);
+        }
       }
     }
     __syncwarp();
@@ -251,12 +312,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // this thread's output feature within the tile
     const int ep = threadIdx.x - 64;      // 0..127
+    if constexpr (KS == 3) {
+      if (helper) {
+        // fp32 partial of all NT tokens -> L2, then publish
+        if (kb1 > kb0) {
+          mbar_wait(&acc_full, 0);
+          tc::fence_after();
+          const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+          float* dstp = a.helper_part + static_cast<size_t>(m) * kHelperPartFloats + row;
+#pragma unroll 1
+          for (int c = 0; c < NT; c += 32) {
+            uint32_t r0[16], r1[16];
+            tc::ld16(lane_addr + c, r0);
+            tc::ld16(lane_addr + c + 16, r1);
+            tc::wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __stcg(dstp + (c + i) * BM, __uint_as_float(r0[i]));
+              __stcg(dstp + (c + 16 + i) * BM, __uint_as_float(r1[i]));
+            }
+          }
+          // the CTA barrier orders every thread's stores before thread 0's
+          // gpu-scope release (cumulativity), so one release publishes them all
+          named_bar_sync(1, 128);
+          if (ep == 0) {
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.helper_flag + m) : "memory");
+            QKV_TRACE(10);
+          }
+        }
+      }
+    }
+    if (!helper) {
     // With a CTA pair each CTA finalises half of the token columns: it sends
     // its partial of the OTHER half to the peer and adds the peer's partial of
     // its own half, so hand-off and stores are split evenly across the pair.
-    constexpr int kHalfNT = KS == 2 ? NT / 2 : NT;
+    constexpr int kHalfNT = KS >= 2 ? NT / 2 : NT;
     const int my_c0 = static_cast<int>(half) * kHalfNT;          // token columns finalised here
-    const int peer_c0 = KS == 2 ? (1 - static_cast<int>(half)) * kHalfNT : 0;
+    const int peer_c0 = KS >= 2 ? (1 - static_cast<int>(half)) * kHalfNT : 0;
     // [kHalfNT][BM] fp32 partial from the peer: its own buffer, or our ring once idle
     float* peer_part = reinterpret_cast<float*>(C::kDedicated ? ring + kRingBytes : ring);
     {
@@ -282,11 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       named_bar_sync(1, 128);
     }
+    float hp[KS == 3 ? kHalfNT : 1];  // KS == 3: the helper's partial of our token half
     mbar_wait(&acc_full, 0);
     tc::fence_after();
     if (ep == 0) QKV_TRACE(6);
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    if constexpr (KS == 2) {
+    if constexpr (KS >= 2) {
       // our MMAs are done, so our ring is free for the peer's partial; once
       // the peer's is free too, asynchronous remote stores of the peer's half
       // straight from the accumulator, completing bytes on its barrier
@@ -318,6 +411,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                        : "memory");
         }
       }
+      if constexpr (KS == 3) {
+        // read from L2 while our st.async hand-off is in flight (the helper
+        // normally published before this CTA's own stream ended)
+        mbar_wait(&helper_ready, 0);
+        const float* srcp = a.helper_part + static_cast<size_t>(m) * kHelperPartFloats + my_c0 * BM + row;
+#pragma unroll
+        for (int i = 0; i < kHalfNT; ++i) hp[i] = __ldcg(srcp + i * BM);
+      }
       mbar_wait(&partial_full, 0);
       if (ep == 0) QKV_TRACE(8);
     }
@@ -333,9 +434,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         v[i] = __uint_as_float(r0[i]);
         v[16 + i] = __uint_as_float(r1[i]);
       }
-      if (KS == 2) {  // two K halves: one fp32 add (commutative, so bit-reproducible)
+      if (KS >= 2) {  // two K halves: one fp32 add (commutative, so bit-reproducible)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] += peer_part[(c + i) * BM + row];
+      }
+      if constexpr (KS == 3) {  // + the helper's k blocks, in a fixed order
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += hp[c + i];
       }
       // transpose through this warp's staging tile (16 tokens x 32
       // features), then 16-byte stores (4 per 64-byte token row segment)
@@ -356,6 +461,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (ep == 0) QKV_TRACE(9);
+    if constexpr (KS == 3) {
+      // both pair CTAs have read the helper's partial: the second resets the flag
+      if (ep == 0 && atomicAdd(a.helper_flag + m, 1) == 2) atomicExch(a.helper_flag + m, 0);
+    }
+    }  // !helper
   }
   tc::fence_before();
   __syncthreads();
@@ -382,11 +492,11 @@ __global__ void pack_weight_kernel(const uint4* __restrict__ w, int hidden, long
 
 template <int NT, int KS>
 int launch(const CUtensorMap& xm, const Args& a, int mtiles, int ttiles, cudaStream_t stream) {
-  const size_t smem = KS == 2 ? Cfg<NT>::kDynSmem : kRingBytes + 1024;
+  const size_t smem = KS >= 2 ? Cfg<NT>::kDynSmem : kRingBytes + 1024;
   static std::atomic<uint64_t> attr_devices{0};
   set_smem_limit_once(qkv_append_kernel<NT, KS>, smem, attr_devices);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(mtiles * KS, ttiles, 1);
+  cfg.gridDim = dim3(KS == 3 ? ((mtiles + 1) / 2 + mtiles) * 2 : mtiles * KS, ttiles, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -394,7 +504,7 @@ int launch(const CUtensorMap& xm, const Args& a, int mtiles, int ttiles, cudaStr
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
   at[0].val.programmaticStreamSerializationAllowed = 1;
   at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = KS;
+  at[1].val.clusterDim.x = KS == 3 ? 2 : KS;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -426,23 +536,48 @@ extern "C" int vt_qkv_pack_weight(const void* w, int32_t feats, int32_t hidden, 
   return cudaGetLastError();
 }
 
+static size_t qkv_flags_bytes(int mtiles) {
+  return (static_cast<size_t>(mtiles) * sizeof(int32_t) + 255) & ~static_cast<size_t>(255);
+}
+
+extern "C" size_t vt_qkv_workspace_bytes(const vt_kv_geometry* g) {
+  const int mtiles = g->q_heads + 2 * g->kv_heads;  // one tile per head (head_dim 128)
+  return qkv_flags_bytes(mtiles) + static_cast<size_t>(mtiles) * kHelperPartFloats * sizeof(float);
+}
+
 extern "C" int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void* x,
                              const void* w_packed, int32_t hidden, int32_t n_tokens,
                              const int32_t* tok_req, const int32_t* tok_pos, const uint64_t* kv_va,
                              void* q_out, int32_t split_k, void* stream) {
+  return vt_qkv_append_ws(g, layer, x, w_packed, hidden, n_tokens, tok_req, tok_pos, kv_va, q_out,
+                          split_k, nullptr, stream);
+}
+
+extern "C" int vt_qkv_append_ws(const vt_kv_geometry* g, int32_t layer, const void* x,
+                                const void* w_packed, int32_t hidden, int32_t n_tokens,
+                                const int32_t* tok_req, const int32_t* tok_pos,
+                                const uint64_t* kv_va, void* q_out, int32_t split_k,
+                                void* workspace, void* stream) {
   if (g->head_dim != 128 || hidden <= 0 || hidden % BK) return cudaErrorInvalidValue;
   if (reinterpret_cast<uintptr_t>(w_packed) & 15) return cudaErrorInvalidValue;
-  if (split_k > 2) return cudaErrorInvalidValue;
+  if (split_k > 3) return cudaErrorInvalidValue;
   if (n_tokens <= 0) return 0;
   const int feats = (g->q_heads + 2 * g->kv_heads) * 128;
   const int mtiles = feats / BM;
   const int kblocks = hidden / BK;
   const int nt = n_tokens <= 64 ? 64 : (n_tokens <= 128 ? 128 : 256);
   const int ttiles = (n_tokens + nt - 1) / nt;
-  // Two CTAs per feature tile (K halves, cluster pair) unless the caller pins
-  // one, or the tile grid alone already covers the SMs several times over.
-  const int ks = split_k > 0 ? split_k : (kblocks >= 2 && mtiles * ttiles < 296 ? 2 : 1);
+  // Auto: with a workspace and one tile of <= 64 tokens (decode), three CTAs
+  // per feature tile (a cluster pair + a helper through L2: 1.5x the SMs
+  // streaming); else two (the K halves on a cluster pair) unless the tile
+  // grid alone already covers the SMs several times over.
+  const bool three_ok = workspace && nt == 64 && ttiles == 1 && kblocks >= 16;
+  const int ks = split_k > 0 ? split_k
+                             : (three_ok ? 3 : (kblocks >= 2 && mtiles * ttiles < 296 ? 2 : 1));
   if (ks == 2 && kblocks < 2) return cudaErrorInvalidValue;
+  // split 3 needs the workspace, one 64-token tile and k blocks for three CTAs
+  if (ks == 3 && (!workspace || nt != 64 || ttiles != 1 || kblocks < 4)) return cudaErrorInvalidValue;
+  if (ks == 3 && (reinterpret_cast<uintptr_t>(workspace) & 255)) return cudaErrorInvalidValue;
 
   CUtensorMap xm;
   {
@@ -465,9 +600,23 @@ extern "C" int vt_qkv_append(const vt_kv_geometry* g, int32_t layer, const void*
   a.layer = layer;
   a.kblocks = kblocks;
   a.chunk_bytes = g->chunk_bytes;
+  a.mtiles = mtiles;
+  if (workspace) {
+    a.helper_flag = static_cast<int32_t*>(workspace);
+    a.helper_part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + qkv_flags_bytes(mtiles));
+  }
+  {
+    static const int helper_q8 = [] {  // helper share of K in 64ths (experiment knob)
+      const char* e = std::getenv("VT_QKV_HELPER_Q64");
+      return e ? std::atoi(e) : 16;
+    }();
+    a.helper_kb = std::max(1, std::min(kblocks - 2, kblocks * helper_q8 / 64));
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rc;
-  if (ks == 2) {
+  if (ks == 3) {
+    rc = launch<64, 3>(xm, a, mtiles, ttiles, s);
+  } else if (ks == 2) {
     rc = nt == 64    ? launch<64, 2>(xm, a, mtiles, ttiles, s)
          : nt == 128 ? launch<128, 2>(xm, a, mtiles, ttiles, s)
                      : launch<256, 2>(xm, a, mtiles, ttiles, s);

@@ -7,8 +7,8 @@ import ctypes
 import pytest
 import torch
 
-from paper_2407_15309_b200.attention import (_Geo, attn_lib, decode_attention, pack_qkv_weight,
-                                             qkv_append)
+from paper_2407_15309_b200.attention import (_Geo, attn_lib, decode_attention,
+                                             pack_qkv_weight, qkv_append, qkv_workspace)
 from paper_2407_15309_b200.kv_layout import KVGeometry
 from vt_gpu_util import admit_with_lengths, cuda_stack
 
@@ -52,8 +52,19 @@ def test_qkv_rejects_contract_violations(cuda_ok):
     x = torch.zeros(2, 4096, dtype=torch.bfloat16, device="cuda")
     tok = torch.arange(2, dtype=torch.int32, device="cuda")
     pw = pack_qkv_weight(w)
-    with pytest.raises(RuntimeError):  # split_k > 2 is not a supported split
-        qkv_append(x, pw, tok, seq, kv_va, st.geo, 0, split_k=3)
+    with pytest.raises(RuntimeError):  # split_k > 3 is not a supported split
+        qkv_append(x, pw, tok, seq, kv_va, st.geo, 0, split_k=4)
+    q = torch.empty(2, 32, 128, dtype=torch.bfloat16, device="cuda")
+    geo = ctypes.byref(_geo())  # the 8B geometry of `st`
+    # split 3 needs a workspace (the plain entry point has none) ...
+    assert lib.vt_qkv_append(geo, 0, x.data_ptr(), pw.data.data_ptr(), 4096, 2, tok.data_ptr(),
+                             seq.data_ptr(), kv_va.data_ptr(), q.data_ptr(), 3, None) != 0
+    # ... and at most 64 tokens
+    x80 = torch.zeros(80, 4096, dtype=torch.bfloat16, device="cuda")
+    ws = qkv_workspace(st.geo)
+    assert lib.vt_qkv_append_ws(geo, 0, x80.data_ptr(), pw.data.data_ptr(), 4096, 80, tok.data_ptr(),
+                                seq.data_ptr(), kv_va.data_ptr(), q.data_ptr(), 3, ws.data_ptr(),
+                                None) != 0
     with pytest.raises(ValueError):  # weight shape does not match the geometry
         qkv_append(x, pack_qkv_weight(torch.zeros(128 * 40, 4096, dtype=torch.bfloat16,
                                                   device="cuda")), tok, seq, kv_va, st.geo, 0)

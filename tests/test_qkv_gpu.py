@@ -30,6 +30,9 @@ CASES = {
     "gqa8_hidden_1024_auto": (16, 2, 16, 1024, [5, 17, 33, 129], 3, 0),
     "llama8b_b100_nt128": (32, 8, 32, 4096, list(range(7, 7 + 100 * 9, 9)), 1, 0),
     "prefill_1000_tokens_multi_segment": (32, 8, 32, 4096, [0, 16, 100, 333], 250, 0),
+    "llama8b_decode_b64_split3": (32, 8, 32, 4096, list(range(3, 3 + 64 * 17, 17)), 1, 3),
+    "gqa8_hidden_1024_split3": (16, 2, 16, 1024, [5, 17, 33, 129], 3, 3),
+    "odd_tile_count_split3": (16, 1, 3, 1024, [5, 17, 300], 2, 3),
 }
 
 
@@ -102,3 +105,65 @@ def test_qkv_append_feeds_decode(cuda_ok):
     out = decode_attention(q, kv_va, torch.tensor(new_lens, dtype=torch.int32, device="cuda"), 7,
                            st.geo, max(new_lens))
     assert rel_err(out.cpu(), ref) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split_k", [2, 3])
+def test_qkv_append_back_to_back_launches(cuda_ok, split_k):
+    """Eight PDL-chained launches on rotating weights (the layer stack's
+    order): every launch's q matches torch — the split-3 helper flags reset
+    inside each launch, and no launch reads another's partials."""
+    layers, hkv, hq, hidden = 32, 8, 32, 4096
+    lens = list(range(3, 3 + 64 * 17, 17))
+    st = cuda_stack(layers, hkv, hq, 4096)
+    kv_va, seq = admit_with_lengths(st, lens, seed=12)
+    for i, n in enumerate(lens):
+        st.sched.extend(f"req{i}", n + 1)
+    st.dev.wait()
+    tok_req = torch.arange(len(lens), device="cuda", dtype=torch.int32)
+    tok_pos = seq.clone()
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    feats = (hq + 2 * hkv) * 128
+    ws = [(torch.randn(feats, hidden, generator=gen, device="cuda") / hidden ** 0.5).to(torch.bfloat16)
+          for _ in range(3)]
+    packed = [pack_qkv_weight(w) for w in ws]
+    xs = [torch.randn(len(lens), hidden, generator=gen, device="cuda").to(torch.bfloat16) for _ in range(8)]
+    outs = [qkv_append(xs[i], packed[i % 3], tok_req, tok_pos, kv_va, st.geo, i % layers, split_k=split_k)
+            for i in range(8)]
+    torch.cuda.synchronize()
+    for i, q in enumerate(outs):
+        ref = (xs[i].float() @ ws[i % 3].float().T).view(-1, hq + 2 * hkv, 128)[:, :hq]
+        assert rel_err(q.float().cpu(), ref.cpu()) <= TOL, f"launch {i}"
+
+
+@pytest.mark.gpu
+def test_qkv_split3_two_streams_concurrently(cuda_ok):
+    """Split 3 keeps its helper partials in a per-stream workspace: launches on
+    two streams at once (different weights, same shape) both match torch."""
+    layers, hkv, hq, hidden = 32, 8, 32, 4096
+    lens = list(range(5, 5 + 48 * 11, 11))
+    st = cuda_stack(layers, hkv, hq, 4096)
+    kv_va, seq = admit_with_lengths(st, lens, seed=13)
+    for i, n in enumerate(lens):
+        st.sched.extend(f"req{i}", n + 1)
+    st.dev.wait()
+    tok_req = torch.arange(len(lens), device="cuda", dtype=torch.int32)
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    feats = (hq + 2 * hkv) * 128
+    ws = [(torch.randn(feats, hidden, generator=gen, device="cuda") / hidden ** 0.5).to(torch.bfloat16)
+          for _ in range(2)]
+    packed = [pack_qkv_weight(w) for w in ws]
+    xs = [torch.randn(len(lens), hidden, generator=gen, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    outs = [[], []]
+    for rep in range(6):
+        for j in range(2):
+            with torch.cuda.stream(streams[j]):
+                outs[j].append(qkv_append(xs[j], packed[j], tok_req, seq, kv_va, st.geo, 2 * rep + j,
+                                          split_k=3, stream=streams[j]))
+    torch.cuda.synchronize()
+    for j in range(2):
+        ref = (xs[j].float() @ ws[j].float().T).view(-1, hq + 2 * hkv, 128)[:, :hq]
+        for q in outs[j]:
+            assert rel_err(q.float().cpu(), ref.cpu()) <= TOL

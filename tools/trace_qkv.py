@@ -37,18 +37,23 @@ qkv_append(x, ws[3], tok_req, tok_pos, kv_va, geo, 0, split_k=split)
 e1.record()
 torch.cuda.synchronize()
 print(f"B={B} split={split} event time {e0.elapsed_time(e1)*1e3:.1f} us")
-buf = (ctypes.c_longlong * (512 * 10))()
+buf = (ctypes.c_longlong * (512 * 12))()
 lib = attn_lib()
 lib.vt_qkv_trace(buf)
-a = np.frombuffer(buf, dtype=np.int64).reshape(512, 10)
-a = a[a[:, 0] > 0]
+a = np.frombuffer(buf, dtype=np.int64).reshape(512, 12)
+n_all = int((a[:, 0] > 0).sum())
+a = a[:n_all]
 t0 = a[:, 0].min()
 names = ["entry", "setup", "w_issue", "first_land", "last_land", "last_commit", "acc_ready",
-         "peer_ready", "partial", "end"]
+         "peer_ready", "partial", "end", "helper_flag"]
 r = a - t0
 r[a == 0] = -1
 print("ctas", len(a))
-for lab, sel in (("lower", np.arange(len(a)) % 2 == 0), ("upper", np.arange(len(a)) % 2 == 1)):
+idx = np.arange(len(a))
+n_help = 2 * ((48 + 1) // 2) if split == 3 else 0  # split 3: helper clusters come first
+groups = [("helper", idx < n_help)] if n_help else []
+groups += [("lower", (idx >= n_help) & (idx % 2 == 0)), ("upper", (idx >= n_help) & (idx % 2 == 1))]
+for lab, sel in groups:
     for j, n in enumerate(names):
         col = r[sel, j]
         col = col[col >= 0]
