@@ -667,6 +667,10 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     wl.gap_events = []
+    # the warm-up's last step ended before the synchronize/barrier above: its
+    # event would turn that host-side pause into a "gap" (and an idle GPU into
+    # a "stall") of the first timed step
+    wl.last_done = None
 
     # ---- device-resident timed region ----
     run_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

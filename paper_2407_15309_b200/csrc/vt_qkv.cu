@@ -98,6 +98,7 @@ struct Args {
   int32_t mtiles, helper_kb;  // KS == 3: feature tiles, k blocks of each tile's helper CTA
   float* helper_part;         // KS == 3 workspace: [mtiles][64 tokens][128] fp32
   int32_t* helper_flag;       //                    [mtiles], zero between launches
+  int32_t l2_prefetch;        // k blocks past the first ring to pull into L2 at entry
 };
 
 // KS == 3 (pair + helper): a third CTA per feature tile streams the first
@@ -121,6 +122,19 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
+// Start-up form: the only cross-CTA state published before it is the
+// mbarrier initialisation, which fence.mbarrier_init.release.cluster already
+// orders, so the arrive can be relaxed (a release arrive also waits for this
+// thread's just-issued weight copies to be translated: ~2 us at launch).
+__device__ __forceinline__ void cluster_sync_init() {
+#ifdef VT_QKV_RELEASE_ARRIVE
+  cluster_sync();
+#else
+  __syncthreads();  // CTA-local: TMEM address and barriers (bar.sync orders shared memory)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+#endif
+}
 // Address of the same shared variable in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
   uint32_t r;
@@ -136,14 +150,17 @@ __device__ __forceinline__ void arrive_peer(uint32_t bar_addr) {
 // 0 entry, 1 setup done, 2 first W copy issued, 3 first stage landed,
 // 4 last stage landed, 5 last MMA committed, 6 accumulator ready,
 // 7 peer handshake done, 8 partial received / sent, 9 epilogue done,
-// 10 (split 3) helper: partial published / pair: helper flag seen.
-__device__ long long g_qkv_trace[512][12];
-__device__ __forceinline__ void trace(int i) {
+// 10 (split 3) helper: partial published / pair: helper flag seen,
+// 11 first ring issued, 12 TMEM allocated, 13 cluster barrier passed,
+// 14 griddepcontrol.wait returned (producer). Two launch slots (layer & 1),
+// so back-to-back launches show on one clock.
+__device__ long long g_qkv_trace[2][256][16];
+__device__ __forceinline__ void trace(int i, int slot) {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  if (blockIdx.y == 0 && blockIdx.x < 512) g_qkv_trace[blockIdx.x][i] = t;
+  if (blockIdx.y == 0 && blockIdx.x < 256) g_qkv_trace[slot & 1][blockIdx.x][i] = t;
 }
-#define QKV_TRACE(i) trace(i)
+#define QKV_TRACE(i) trace(i, a.layer)
 #else
 #define QKV_TRACE(i)
 #endif
@@ -221,14 +238,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                kBlockBytes, &full[i], once);
       if (i == 0) QKV_TRACE(2);
     }
+    // The next blocks into L2 as well: this CTA becomes resident as the
+    // previous launch's CTAs leave, so these reads fill the HBM gap of that
+    // launch's tail and of the dependency wait (x, hence the MMAs, only
+    // arrive after griddepcontrol.wait).
+    for (int i = C::kStages; i < min(n, C::kStages + a.l2_prefetch); ++i)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wsrc + static_cast<uint64_t>(i) * kBlockBytes),
+                   "r"(kBlockBytes)
+                   : "memory");
+    QKV_TRACE(11);
   }
   if (warp == 1) tc::alloc(&tmem_base, C::kTmemCols);
+  if (threadIdx.x == 32) QKV_TRACE(12);
   tc::fence_before();
   if constexpr (KS >= 2) {
-    cluster_sync();  // the peer's barriers are initialised before any remote arrive
+    cluster_sync_init();  // the peer's barriers are initialised before any remote arrive
   } else {
     __syncthreads();
   }
+  if (threadIdx.x == 0) QKV_TRACE(13);
   tc::fence_after();
   const uint32_t tmem = tmem_base;
   tc::grid_launch_dependents();  // the next launch may start its own prologue
@@ -251,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // griddepcontrol.wait.
       const int pre = min(n, C::kStages);  // issued at barrier init
       tc::grid_dependency_wait();
+      QKV_TRACE(14);
       for (int i = 0; i < n; ++i) {
         const int st = i % C::kStages;
         uint8_t* sw = ring + st * C::kStageBytes;
@@ -611,6 +640,11 @@ extern "C" int vt_qkv_append_ws(const vt_kv_geometry* g, int32_t layer, const vo
       return e ? std::atoi(e) : 16;
     }();
     a.helper_kb = std::max(1, std::min(kblocks - 2, kblocks * helper_q8 / 64));
+    static const int l2_pf = [] {  // k blocks past the ring prefetched into L2 (A/B knob)
+      const char* e = std::getenv("VT_QKV_L2_PREFETCH");
+      return e ? std::atoi(e) : 4;  // r2as sweep at B=64: 0/4/8/16/64 -> 10.60/10.34/10.40/10.77/10.77 us
+    }();
+    a.l2_prefetch = ttiles == 1 ? l2_pf : 0;  // several token tiles re-read W from L2 anyway
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rc;
