@@ -99,6 +99,7 @@ struct Args {
   float* helper_part;         // KS == 3 workspace: [mtiles][64 tokens][128] fp32
   int32_t* helper_flag;       //                    [mtiles], zero between launches
   int32_t l2_prefetch;        // k blocks past the first ring to pull into L2 at entry
+  int32_t l2_prefetch_helper; // the same for KS == 3 helper CTAs
 };
 
 // KS == 3 (pair + helper): a third CTA per feature tile streams the first
@@ -242,7 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // previous launch's CTAs leave, so these reads fill the HBM gap of that
     // launch's tail and of the dependency wait (x, hence the MMAs, only
     // arrive after griddepcontrol.wait).
-    for (int i = C::kStages; i < min(n, C::kStages + a.l2_prefetch); ++i)
+    const int pf = helper ? a.l2_prefetch_helper : a.l2_prefetch;
+    for (int i = C::kStages; i < min(n, C::kStages + pf); ++i)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wsrc + static_cast<uint64_t>(i) * kBlockBytes),
                    "r"(kBlockBytes)
                    : "memory");
@@ -644,7 +646,12 @@ extern "C" int vt_qkv_append_ws(const vt_kv_geometry* g, int32_t layer, const vo
       const char* e = std::getenv("VT_QKV_L2_PREFETCH");
       return e ? std::atoi(e) : 4;  // r2as sweep at B=64: 0/4/8/16/64 -> 10.60/10.34/10.40/10.77/10.77 us
     }();
+    static const int l2_pf_helper = [] {
+      const char* e = std::getenv("VT_QKV_L2_PREFETCH_HELPER");
+      return e ? std::atoi(e) : -1;
+    }();
     a.l2_prefetch = ttiles == 1 ? l2_pf : 0;  // several token tiles re-read W from L2 anyway
+    a.l2_prefetch_helper = l2_pf_helper >= 0 && ttiles == 1 ? l2_pf_helper : a.l2_prefetch;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rc;
