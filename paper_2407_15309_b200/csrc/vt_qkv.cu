@@ -285,12 +285,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < n; ++i) {
         const int st = i % C::kStages;
         uint8_t* sw = ring + st * C::kStageBytes;
+#ifdef VT_QKV_EXP_NOX  // timing experiment only (wrong results): x read in the first ring only
+        if (i >= pre) {
+          mbar_wait(&empty[st], ((i / C::kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], kBlockBytes);
+          bulk_g2s(sw, wsrc + static_cast<uint64_t>(i) * kBlockBytes, kBlockBytes, &full[st], once);
+        } else {
+          tc::tma_load_2d(sw + kBlockBytes, &x_map, &full[st], (kb0 + i) * BK, tt * NT, keep);
+        }
+#else
         if (i >= pre) {
           mbar_wait(&empty[st], ((i / C::kStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[st], C::kStageBytes);
           bulk_g2s(sw, wsrc + static_cast<uint64_t>(i) * kBlockBytes, kBlockBytes, &full[st], once);
         }
         tc::tma_load_2d(sw + kBlockBytes, &x_map, &full[st], (kb0 + i) * BK, tt * NT, keep);
+#endif
       }
       if constexpr (KS == 3) {
         // the producer is idle from here: it watches for the helper's partial
