@@ -186,11 +186,9 @@ def dist_setup(args):
     the N-rank mechanics on a 1-GPU box) ranks share devices round-robin, the
     timing reductions go over gloo (NCCL refuses two ranks on one GPU);
     numbers from such a run are not scaling numbers — a mechanics check only,
-    never the driver's one-rank-per-GPU configuration. Two processes' tcgen05
-    /TMEM kernels time-sliced on one GPU stall (r02 bisect: tcgen05 decode
-    hung 4 of 4 two-rank runs, chained or not; the CUDA-core decode, which
-    holds no TMEM, completed 2 of 2), so an oversubscribed run uses the
-    CUDA-core path and says so in its config."""
+    never the driver's one-rank-per-GPU configuration. (Two ranks' tcgen05
+    decode kernels time-sliced on one GPU used to deadlock on an mbarrier
+    parity race, fixed in r02: tests/test_timeslice_gpu.py.)"""
     global _COLL_DEVICE
     import torch
 
@@ -208,11 +206,8 @@ def dist_setup(args):
         else:
             dist.init_process_group("gloo")
             _COLL_DEVICE = "cpu"
-            if args.path == "tcgen05":
-                args.path = "cuda_core"
-                args.oversubscribed = ("%d ranks share %d GPU(s): decode on the CUDA-core path "
-                                       "(time-sliced tcgen05/TMEM kernels of two processes stall)"
-                                       % (world, n_dev))
+            args.oversubscribed = ("%d ranks share %d GPU(s): time-sliced, a mechanics check, "
+                                   "not a scaling number" % (world, n_dev))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, torch.cuda.current_device() if torch.cuda.is_available() else local

@@ -39,6 +39,39 @@
 namespace vt {
 namespace dtc {
 
+#ifdef VT_DTC_HANG_DEBUG
+// Debug build (tools/hang_probe_decode.py): an mbarrier wait that has not
+// completed after 2 s records (source line, CTA, thread, parity, raw barrier
+// word) into host-mapped memory once, then keeps waiting, so a hung process
+// can say which wait it is stuck in.
+__device__ unsigned long long* g_dbg;
+__device__ void dbg_wait(uint64_t* bar, uint32_t parity, int line) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  bool recorded = false;
+  while (!mbar_try_wait(bar, parity)) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!recorded && t - t0 > 2000000000ull && g_dbg) {
+      recorded = true;
+      const unsigned long long i = atomicAdd(g_dbg, 1ull);
+      if (i < 256) {
+        unsigned long long raw;
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(smem_u32(bar)));
+        volatile unsigned long long* r = g_dbg + 1 + i * 6;
+        r[0] = line;
+        r[1] = blockIdx.x;
+        r[2] = threadIdx.x;
+        r[3] = parity;
+        r[4] = raw;
+        r[5] = smem_u32(bar);
+        __threadfence_system();
+      }
+    }
+  }
+}
+#define mbar_wait(b, p) dbg_wait((b), (p), __LINE__)
+#endif
+
 constexpr int TILE = 128;   // tokens per KV tile (MMA M)
 constexpr int D = 128;
 constexpr int NQ = 16;      // padded q-head columns (MMA N)
@@ -68,8 +101,14 @@ struct __align__(1024) Smem {
   uint64_t v_full[VSTAGES], v_empty[VSTAGES];
   uint64_t q_full[2], q_empty[2];
   uint64_t s_full[2];
-  uint64_t p_full;
-  uint64_t pv_done[2];  // by tile parity: a waiter can never fall two phases behind
+  // By tile parity: a waiter can never fall two phases behind. (A single
+  // p_full let the softmax arrive P(g) — S(g) is issued before the MMA warp
+  // waits for P(g-1) — before the MMA warp had observed P(g-1)'s phase; the
+  // barrier then read as pending again and the two roles deadlocked. Seen
+  // only when a time-sliced second process delayed the MMA warp, r02:
+  // tools/hang_probe_decode.py, profiles/r02/timeslice/.)
+  uint64_t p_full[2];
+  uint64_t pv_done[2];
   uint64_t epi_full[2], epi_empty[2];
   uint32_t tmem_base;
 };
@@ -159,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_empty[i], 1);
       mbar_init(&sm.s_full[i], 1);
     }
-    mbar_init(&sm.p_full, 128);
+    mbar_init(&sm.p_full[0], 128);
+    mbar_init(&sm.p_full[1], 128);
     mbar_init(&sm.pv_done[0], 1);
     mbar_init(&sm.pv_done[1], 1);
     for (int i = 0; i < 2; ++i) {
@@ -240,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = 0;   // global tile counter (S/P/PV phases)
       int qc = 0;
       auto issue_pv = [&](int gt) {
-        mbar_wait(&sm.p_full, gt & 1);
+        mbar_wait(&sm.p_full[gt & 1], (gt >> 1) & 1);
         const int vs = gt % VSTAGES;
         mbar_wait(&sm.v_full[vs], (gt / VSTAGES) & 1);
         tc::fence_after();
@@ -476,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         tc::fence_before();
-        mbar_arrive(&sm.p_full);
+        mbar_arrive(&sm.p_full[g & 1]);
         if (g > g_first) fold(g - 1);
 #pragma unroll
         for (int c = 0; c < G; ++c) alpha_prev[c] = alpha[c];
@@ -506,6 +546,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace vt
 
 using namespace vt::dtc;
+
+#ifdef VT_DTC_HANG_DEBUG
+extern "C" int vt_dtc_debug_set(unsigned long long* host_mapped) {
+  return cudaMemcpyToSymbol(g_dbg, &host_mapped, sizeof(host_mapped));
+}
+#endif
 
 // Called from vt_decode.cu's dispatcher (same workspace layout as the CUDA-core
 // path, so the combine kernel is shared).

@@ -6,7 +6,8 @@ owns its own ``VirtualMemoryDevice`` (its own VMM chunk pool and VA ranges),
 manager and kernel launches; no collective touches the data path — gloo only
 gathers the per-rank outputs so rank 0 can check them. The round-end box has
 one GPU, so ranks map onto ``cuda:(rank % device_count)`` and take turns on it
-(two processes' tcgen05 kernels time-sliced on one GPU were seen to stall);
+(concurrent time-sliced ranks are covered, under a hard timeout, by
+test_timeslice_gpu.py);
 the N pools share its HBM, which changes nothing on the path under test
 (every pool, VA and launch is still private to its rank).
 
@@ -126,9 +127,9 @@ def _rank_main(rank, world, port, tmp):
             return out
 
         # Ranks share the one GPU here: they run their GPU sections one after
-        # another (gloo barriers), so no two contexts' tcgen05 kernels are
-        # time-sliced against each other; everything else (process, VMM pool,
-        # VA ranges, manager, launches) stays private to each rank.
+        # another (gloo barriers) so a spawn without a timeout can never wait
+        # on a wedged peer; everything else (process, VMM pool, VA ranges,
+        # manager, launches) stays private to each rank.
         results = None
         for turn in range(world):
             if turn == rank:
