@@ -494,7 +494,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = lane; j < 64; j += 32) {
           const uint64_t dst = row_dst[my_c0 + c + h * 16 + (j >> 2)];
+#if defined(VT_QKV_EXP_NOKV)  // timing experiments only: skip the K/V row stores
+          if (dst && m < a.hq)
+#elif defined(VT_QKV_EXP_NOSTORE)  // ... or every row store
+          if (dst && m < 0)
+#else
           if (dst)
+#endif
             *reinterpret_cast<uint4*>(dst + quarter * 64 + (j & 3) * 16) =
                 *reinterpret_cast<const uint4*>(&stage_out[quarter][j >> 2][(j & 3) * 8]);
         }

@@ -1,7 +1,7 @@
 # r2au (late round 2): GPU suite, smoke, default bench line, reference arm, a
 # 2-rank run, and ncu --set full of the fused QKV kernel (split 3, new start-up).
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2au; mkdir -p $O
+O=gpurun_out/${RUN:-r2au}; mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -1 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?; tail -1 $O/smoke.log
 timeout 400 python bench.py > $O/bench.log 2>&1; echo bench rc=$?
