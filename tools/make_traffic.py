@@ -1,6 +1,6 @@
 """Write profiles/decode_traffic.json — roofline.traffic per bench config —
 from `ncu --set full` captures of ONE decode launch inside `bench.py
---profile-steps` for each config (tools/gpu_r2j.sh).
+--profile-steps` for each config (tools/gpu_r2j.sh; late r02 recapture: tools/gpu_r2be.sh).
 
     python tools/make_traffic.py gpurun_out/r2j > profiles/decode_traffic.json
 
@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 def main(d: str) -> None:
     out = {"note": ("dram__bytes_read.sum + dram__bytes_write.sum of one decode launch, from an "
                     "`ncu --set full --clock-control none` capture inside `bench.py --config C "
-                    "--profile-steps 3` (tools/gpu_r2j.sh); one launch = one layer of the config's "
+                    "--profile-steps 3` (tools/gpu_r2j.sh; late r02 recapture: tools/gpu_r2be.sh); one launch = one layer of the config's "
                     "batch at its context")}
     for rep in sorted(glob.glob(os.path.join(d, "decode_*.ncu-rep"))):
         key = os.path.basename(rep)[len("decode_"):-len(".ncu-rep")].replace("__", "/")
@@ -29,7 +29,7 @@ def main(d: str) -> None:
                                       capture_output=True, text=True, check=True).stdout)
         out[key] = {"kernel": s.get("kernel"), "dram_bytes_per_launch": int(s["dram_traffic_bytes"]),
                     "duration_us": round(s["duration"] * 1e6, 2),
-                    "source": f"profiles/r02/ncu/{os.path.basename(rep)[:-8]}.json"}
+                    "source": f"profiles/r02/ncu_late/{os.path.basename(rep)[:-8]}.json"}
     print(json.dumps(out, indent=1))
 
 
