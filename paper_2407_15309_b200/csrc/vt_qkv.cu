@@ -69,7 +69,10 @@ constexpr int BM = 128;  // output features per tile
 constexpr int BK = 64;   // hidden elements per k block (one 128-byte SW128 row)
 constexpr int kBlockBytes = BM * BK * 2;  // one packed weight block (16 KiB)
 constexpr int kThreads = 192;
-constexpr int kRingBytes = 192 * 1024;
+#ifndef VT_QKV_RING_KB
+#define VT_QKV_RING_KB 192  // (timing experiments override it: ring-depth sensitivity)
+#endif
+constexpr int kRingBytes = VT_QKV_RING_KB * 1024;
 
 template <int NT>
 struct Cfg {
