@@ -288,22 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < n; ++i) {
         const int st = i % C::kStages;
         uint8_t* sw = ring + st * C::kStageBytes;
-#ifdef VT_QKV_EXP_NOX  // timing experiment only (wrong results): x read in the first ring only
-        if (i >= pre) {
-          mbar_wait(&empty[st], ((i / C::kStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[st], kBlockBytes);
-          bulk_g2s(sw, wsrc + static_cast<uint64_t>(i) * kBlockBytes, kBlockBytes, &full[st], once);
-        } else {
-          tc::tma_load_2d(sw + kBlockBytes, &x_map, &full[st], (kb0 + i) * BK, tt * NT, keep);
-        }
-#else
         if (i >= pre) {
           mbar_wait(&empty[st], ((i / C::kStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[st], C::kStageBytes);
           bulk_g2s(sw, wsrc + static_cast<uint64_t>(i) * kBlockBytes, kBlockBytes, &full[st], once);
         }
         tc::tma_load_2d(sw + kBlockBytes, &x_map, &full[st], (kb0 + i) * BK, tt * NT, keep);
-#endif
       }
       if constexpr (KS == 3) {
         // the producer is idle from here: it watches for the helper's partial
@@ -497,13 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = lane; j < 64; j += 32) {
           const uint64_t dst = row_dst[my_c0 + c + h * 16 + (j >> 2)];
-#if defined(VT_QKV_EXP_NOKV)  // timing experiments only: skip the K/V row stores
-          if (dst && m < a.hq)
-#elif defined(VT_QKV_EXP_NOSTORE)  // ... or every row store
-          if (dst && m < 0)
-#else
           if (dst)
-#endif
             *reinterpret_cast<uint4*>(dst + quarter * 64 + (j & 3) * 16) =
                 *reinterpret_cast<const uint4*>(&stage_out[quarter][j >> 2][(j & 3) * 8]);
         }
